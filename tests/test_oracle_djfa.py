@@ -1,0 +1,129 @@
+"""Pins for the oracle's dJFA step (Alg. 1; Eq. 3-4) and the seed move.
+
+Independent references: the hand-worked fixture tests/golden/djfa_4x4_step.txt,
+closed-form special cases (zero motion from an exact diagram, one seed, clamping),
+the exact diagram (Eq. 1), and the paper's similarity trend ("nearly 100%").
+"""
+import numpy as np
+import pytest
+
+import golden_io
+import oracle
+import synth
+
+EMPTY = 0xFFFFFFFF
+
+
+def test_golden_djfa_step():
+    fx = golden_io.load("djfa_4x4_step.txt")
+    N = fx["N"]
+    old = golden_io.seeds_xy(fx, "prev_seeds")
+    disp = golden_io.disp_xy(fx)
+    new = golden_io.seeds_xy(fx, "seeds")
+    assert oracle.djfa_schedule(N, 2, fx["d_max"]) == fx["schedule"]
+    assert np.array_equal(oracle.move(N, old, disp), new)
+    prev = golden_io.grid(fx, "prev")
+    assert np.array_equal(oracle.exact_brute(N, old), prev)
+    G, xy_new, n = oracle.djfa_step(N, old, disp, fx["d_max"], prev)
+    assert n == 2 and np.array_equal(xy_new, new)
+    assert np.array_equal(G, golden_io.grid(fx, "final"))
+    # the intermediate grids, reproduced with the oracle's own pass
+    remapped = golden_io.grid(fx, "after_remap")
+    assert np.array_equal(oracle.jump_pass(remapped, 2), golden_io.grid(fx, "after_k2"))
+
+
+def test_move_clamps_per_axis():
+    # R-10: clamp, not wrap; per axis.
+    old = np.array([0, 0, 7, 7, 3, 4], dtype=np.uint16)
+    disp = np.array([-1, -5, 1, 9, 2, -2], dtype=np.int16)
+    assert np.array_equal(oracle.move(8, old, disp), np.array([0, 0, 7, 7, 5, 2], dtype=np.uint16))
+
+
+def test_move_reserved_pixel_at_65536():
+    # R-4: at N = 65536 the pixel (65535, 65535) is the EMPTY sentinel and is reserved.
+    old = np.array([65534, 65535, 65535, 65534, 65535, 65535 - 3], dtype=np.uint16)
+    disp = np.array([1, 0, 0, 1, 5, 5], dtype=np.int16)
+    new = oracle.move(65536, old, disp)
+    assert new.tolist() == [65534, 65535, 65534, 65535, 65534, 65535]
+    # not applied below 65536
+    assert oracle.move(65535, np.array([65533, 65533], dtype=np.uint16),
+                       np.array([1, 1], dtype=np.int16)).tolist() == [65534, 65534]
+
+
+@pytest.mark.parametrize("N,s", [(16, 4), (64, 16), (100, 37)])
+def test_zero_motion_from_exact_is_identity(N, s):
+    # no seed moved and prev exact -> unchanged (exact is a fixed point of every
+    # pass; fwd is the identity; re-stamping writes labels already present).
+    xy = synth.uniform_seeds(N, s, rng_seed=N + s)
+    E = oracle.exact_brute(N, xy)
+    G, xy_new, _ = oracle.djfa_step(N, xy, np.zeros(2 * s, dtype=np.int16), 1, E)
+    assert np.array_equal(G, E) and np.array_equal(xy_new, xy)
+
+
+def test_one_seed_follows_its_seed():
+    # 1 seed after any move -> every pixel holds it.
+    N = 32
+    xy = np.array([5, 9], dtype=np.uint16)
+    G = oracle.jfa(N, xy)
+    for f in range(5):
+        d = synth.displacements(1, 7, f, rng_seed=3)
+        G, xy, _ = oracle.djfa_step(N, xy, d, 7, G)
+        assert (G == oracle.pack(int(xy[0]), int(xy[1]))).all()
+
+
+def test_rejects_incomplete_prev():
+    # run_djfa_step rejects an incomplete previous diagram.
+    N = 8
+    xy = np.array([1, 1, 6, 6], dtype=np.uint16)
+    G = oracle.jfa(N, xy)
+    G[0, 0] = EMPTY
+    with pytest.raises(ValueError):
+        oracle.djfa_step(N, xy, np.zeros(4, dtype=np.int16), 1, G)
+    G = oracle.jfa(N, xy)
+    G[0, 0] = oracle.pack(3, 3)  # not a seed
+    with pytest.raises(ValueError):
+        oracle.djfa_step(N, xy, np.zeros(4, dtype=np.int16), 1, G)
+
+
+def test_labels_follow_seeds_and_restamp():
+    # R-9: after a step every label is a NEW seed position and every new seed pixel holds
+    # itself -- including co-located seeds that split up (min packed new position wins
+    # the old pixel, the other is re-stamped).
+    N = 16
+    old = np.array([4, 4, 4, 4, 12, 12], dtype=np.uint16)
+    G = oracle.exact_brute(N, old)
+    disp = np.array([3, 0, -3, 0, 0, 1], dtype=np.int16)
+    H, new, _ = oracle.djfa_step(N, old, disp, 3, G)
+    labels = {oracle.pack(int(new[2 * i]), int(new[2 * i + 1])) for i in range(3)}
+    assert set(np.unique(H).tolist()) <= labels
+    for c in labels:
+        assert H[c >> 16, c & 0xFFFF] == c
+
+
+def _simulate(N, s, d, frames, seed):
+    xy = synth.uniform_seeds(N, s, rng_seed=seed)
+    G = oracle.jfa(N, xy)
+    out = []
+    for f in range(frames):
+        disp = synth.displacements(s, d, f, rng_seed=seed)
+        G, xy, _ = oracle.djfa_step(N, xy, disp, d, G)
+        out.append((G.copy(), xy.copy()))
+    return out
+
+
+def test_djfa_similarity_c1():
+    # Config C1 of BASELINE.json: 64x64, 16 seeds, 10 steps.  P:268: dJFAe is "nearly
+    # 100%" similar to JFA; SPEC AC3 asks >= 95%.  Also vs exact.
+    for G, xy in _simulate(64, 16, 1, 10, 2209):
+        J = oracle.jfa(64, xy)
+        E = oracle.exact_brute(64, xy)
+        assert oracle.similarity(G, J) >= 95.0
+        assert oracle.similarity(G, E) >= 95.0
+        assert (G != EMPTY).all()
+
+
+def test_djfa_similarity_denser():
+    sims = []
+    for G, xy in _simulate(256, 256, 4, 6, 7):
+        sims.append(oracle.similarity(G, oracle.jfa(256, xy)))
+    assert min(sims) >= 95.0 and np.mean(sims) >= 99.0
