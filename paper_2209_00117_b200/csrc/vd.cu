@@ -1,0 +1,832 @@
+// vd.cu -- libvd: host runtime + C ABI (include/vd.h) of the B200 dJFA hot path.
+//
+// One handle = one diagram on one GPU (or one rank's row band).  The handle owns every
+// device buffer; work is enqueued on one CUDA stream (the caller's, e.g. torch's current
+// stream, or its own).  Multi-GPU halo exchange uses NCCL point-to-point calls, loaded
+// at run time with dlopen (the library itself does not link NCCL).
+//
+// "P:n" = line n of the paper's LaTeX source; "R-n" = reading n in DESIGN.md §3.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vd.h"
+#include "vd_kernels.cuh"
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+  bool tried = false, ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+
+bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) { g_nccl.err = std::string("dlopen libnccl.so.2 failed: ") + dlerror(); return false; }
+#define VD_SYM(field, name)                                                   \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));    \
+  if (!g_nccl.field) { g_nccl.err = std::string("missing symbol ") + name; return false; }
+  VD_SYM(GetUniqueId, "ncclGetUniqueId");
+  VD_SYM(CommInitRank, "ncclCommInitRank");
+  VD_SYM(CommDestroy, "ncclCommDestroy");
+  VD_SYM(GroupStart, "ncclGroupStart");
+  VD_SYM(GroupEnd, "ncclGroupEnd");
+  VD_SYM(Send, "ncclSend");
+  VD_SYM(Recv, "ncclRecv");
+  VD_SYM(AllReduce, "ncclAllReduce");
+  VD_SYM(GetErrorString, "ncclGetErrorString");
+#undef VD_SYM
+  g_nccl.ok = true;
+  return true;
+}
+
+// ------------------------------------------------------------------ schedules (host)
+uint32_t ceil_log2_u64(uint64_t n) {
+  uint32_t e = 0;
+  while ((1ull << e) < n) ++e;
+  return e;
+}
+
+// Eq. 2, R-5: k_1 = 2^(ceil(log2 N) - 1), halving to 1, + extras (R-6).
+int schedule_jfa(uint32_t N, uint32_t extras, std::vector<uint32_t>& ks) {
+  ks.clear();
+  if (N < 2) return -1;
+  for (uint32_t k = 1u << (ceil_log2_u64(N) - 1); k >= 1; k >>= 1) ks.push_back(k);
+  for (uint32_t i = 0; i < extras; ++i) ks.push_back(1);
+  return 0;
+}
+
+// Eq. 3-4 in exact integers (R-7): delta_1 = 2^e with
+// e = min(max(e_L, e_d), log2 k_1), e_L = min{e : s 4^e >= 4 N^2}, e_d = ceil(log2 d_max).
+int schedule_djfa(uint32_t N, uint64_t s, uint32_t d_max, uint32_t extras, std::vector<uint32_t>& ks) {
+  ks.clear();
+  if (N < 2 || s == 0) return -1;
+  const unsigned __int128 target = (unsigned __int128)4 * N * N;
+  uint32_t eL = 0;
+  while (((unsigned __int128)s << (2 * eL)) < target) ++eL;
+  const uint32_t ed = d_max <= 1 ? 0 : ceil_log2_u64(d_max);
+  uint32_t e = std::max(eL, ed);
+  e = std::min(e, ceil_log2_u64(N) - 1);
+  for (int i = (int)e; i >= 0; --i) ks.push_back(1u << i);
+  for (uint32_t i = 0; i < extras; ++i) ks.push_back(1);
+  return 0;
+}
+
+void halo_plan(uint32_t N, uint32_t world, uint32_t rank, uint32_t k, vd_halo_plan_t& p) {
+  const uint32_t B = N / world;
+  const uint32_t d = (k + B - 1) / B;
+  const uint32_t h = std::min(k, B);
+  p.halo_rows = h;
+  p.recv_top_rank = (int64_t)rank - (int64_t)d >= 0 ? (int32_t)(rank - d) : -1;
+  p.recv_bot_rank = (uint64_t)rank + d < world ? (int32_t)(rank + d) : -1;
+  p.top_row0 = (int64_t)rank * B - (int64_t)k;
+  p.bot_row0 = (int64_t)rank * B + (int64_t)d * B;
+  p.send_top_row0 = 0;
+  p.send_bot_row0 = B - h;
+}
+
+struct Shard {
+  uint32_t row0 = 0, rows = 0;
+  uint32_t* buf[2] = {nullptr, nullptr};  // ping-pong diagrams, rows x pitch
+  uint32_t* top = nullptr;                // halo from the band above, hcap x pitch
+  uint32_t* bot = nullptr;                // halo from the band below
+};
+
+}  // namespace
+
+struct vd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint32_t N = 0;
+  uint64_t s = 0;
+  int64_t pitch = 0;
+  int rank = 0, world = 1;
+  uint32_t vshards = 1;
+  uint32_t extras = 0;
+  uint32_t hcap = 0;  // halo rows allocated per side
+  std::vector<Shard> shards;
+  int cur = 0;        // which ping-pong buffer holds the diagram
+  bool has_diagram = false;
+  uint32_t* seeds = nullptr;      // [s] current positions (labels)
+  uint32_t* seeds_new = nullptr;  // [s] scratch for the move
+  short2* disp = nullptr;         // [s] displacements on device
+  short2* disp_stage = nullptr;   // [s] pinned host staging
+  cudaEvent_t disp_done = nullptr;
+  uint32_t* fwd = nullptr;        // [N*N] forward map (dJFA), allocated on first use
+  unsigned long long* counter = nullptr;     // device u64 for reductions
+  unsigned long long* counter_h = nullptr;   // pinned host copy
+  uint32_t last_passes = 0;
+  uint64_t launches = 0;
+  vd_status sticky = VD_OK;
+  std::string err;
+  // instrumentation
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  uint64_t timed_px = 0, timed_launches = 0;
+  // NCCL
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+vd_status fail(vd_ctx* h, vd_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) {
+    if (st == VD_ERR_CUDA || st == VD_ERR_NCCL) h->sticky = st;
+    h->err = buf;
+  }
+  return st;
+}
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(h, e_ == cudaErrorMemoryAllocation ? VD_ERR_OOM : VD_ERR_CUDA, \
+                                       "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define CKN(expr)                                                                             \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess) return fail(h, VD_ERR_NCCL, "%s: %s", #expr, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+#define CHECK_HANDLE(h)                        \
+  do {                                         \
+    if (!(h)) return VD_ERR_ARG;               \
+    if ((h)->sticky != VD_OK) return (h)->sticky; \
+  } while (0)
+
+int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+vd_status after_launch(vd_ctx* h, const char* what) {
+  h->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, VD_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return VD_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Copy s displacement pairs (host or device) to h->disp, asynchronously and safely: host
+// data goes through the handle's pinned staging buffer, so the caller may reuse its array
+// as soon as the call returns.
+vd_status upload_disp(vd_ctx* h, const int16_t* disp_xy) {
+  const size_t bytes = h->s * sizeof(short2);
+  if (is_device_ptr(disp_xy)) {
+    CK(cudaMemcpyAsync(h->disp, disp_xy, bytes, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    CK(cudaEventSynchronize(h->disp_done));  // previous upload out of the staging buffer
+    memcpy(h->disp_stage, disp_xy, bytes);
+    CK(cudaMemcpyAsync(h->disp, h->disp_stage, bytes, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaEventRecord(h->disp_done, h->stream));
+  }
+  return VD_OK;
+}
+
+vd_status timed_begin(vd_ctx* h) {
+  if (!h->timing) return VD_OK;
+  while (h->ev.size() < h->ev_used + 2) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->ev.push_back(e);
+  }
+  CK(cudaEventRecord(h->ev[h->ev_used], h->stream));
+  return VD_OK;
+}
+vd_status timed_end(vd_ctx* h, uint64_t px) {
+  if (!h->timing) return VD_OK;
+  CK(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+  h->ev_used += 2;
+  h->timed_px += px;
+  h->timed_launches++;
+  return VD_OK;
+}
+
+// Which kernel variant can take this pass exactly (see vd_kernels.cuh).
+bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
+
+vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
+  vdk::PassArgs a;
+  a.in = sh.buf[h->cur];
+  a.out = sh.buf[h->cur ^ 1];
+  a.top = sh.top;
+  a.bot = sh.bot;
+  a.pitch = h->pitch;
+  a.N = (int)h->N;
+  a.row0 = (int)sh.row0;
+  a.rows = (int)sh.rows;
+  const uint32_t B = sh.rows;
+  const uint32_t d = (k + B - 1) / B;
+  a.top_row0 = (int)sh.row0 - (int)k;
+  a.bot_row0 = (int)(sh.row0 + d * B);
+  a.k = (int)k;
+  a.xblocks = (int)((h->N + 4 * vdk::kThreads - 1) / (4 * vdk::kThreads));
+  const uint32_t C = 2 * h->N - 1;
+  a.vempty = (C << 16) | C;
+  a.sh16 = 65536u;
+  vd_status st = timed_begin(h);
+  if (st) return st;
+  if (fast_ok(h->N, may_empty) && (k & (k - 1)) == 0) {
+    const uint32_t nres = std::min(k, B);
+    const uint32_t per_res = (B + k - 1) / k;
+    a.segs = (int)((per_res + vdk::kWalk - 1) / vdk::kWalk);
+    const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
+    const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
+    const bool banded = sh.top != nullptr;
+#define VD_LAUNCH(KM)                                                                        \
+  do {                                                                                       \
+    if (may_empty) {                                                                         \
+      if (banded) vdk::jump_pass_fast<KM, true, true><<<grid, blk, 0, h->stream>>>(a);      \
+      else vdk::jump_pass_fast<KM, true, false><<<grid, blk, 0, h->stream>>>(a);            \
+    } else {                                                                                 \
+      if (banded) vdk::jump_pass_fast<KM, false, true><<<grid, blk, 0, h->stream>>>(a);     \
+      else vdk::jump_pass_fast<KM, false, false><<<grid, blk, 0, h->stream>>>(a);           \
+    }                                                                                        \
+  } while (0)
+    if (k == 1) VD_LAUNCH(1);
+    else if (k == 2) VD_LAUNCH(2);
+    else VD_LAUNCH(4);
+#undef VD_LAUNCH
+  } else {
+    a.segs = 1;
+    const int64_t blocks = (int64_t)a.xblocks * B;
+    vdk::jump_pass_wide<<<dim3((unsigned)blocks), dim3(vdk::kThreads), 0, h->stream>>>(a);
+  }
+  st = after_launch(h, "jump_pass");
+  if (st) return st;
+  return timed_end(h, (uint64_t)B * h->N);
+}
+
+// Halo exchange for step k (vd_halo_plan), then one pass on every local shard.
+vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty) {
+  const size_t row_bytes = (size_t)h->pitch * sizeof(uint32_t);
+  if (h->world > 1) {
+    vd_halo_plan_t p;
+    halo_plan(h->N, (uint32_t)h->world, (uint32_t)h->rank, k, p);
+    Shard& sh = h->shards[0];
+    const size_t cnt = (size_t)p.halo_rows * h->pitch;
+    CKN(g_nccl.GroupStart());
+    if (p.recv_top_rank >= 0) {
+      CKN(g_nccl.Recv(sh.top, cnt, ncclUint32, p.recv_top_rank, h->comm, h->stream));
+      CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_top_row0 * h->pitch, cnt, ncclUint32, p.recv_top_rank, h->comm, h->stream));
+    }
+    if (p.recv_bot_rank >= 0) {
+      CKN(g_nccl.Recv(sh.bot, cnt, ncclUint32, p.recv_bot_rank, h->comm, h->stream));
+      CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_bot_row0 * h->pitch, cnt, ncclUint32, p.recv_bot_rank, h->comm, h->stream));
+    }
+    CKN(g_nccl.GroupEnd());
+  } else if (h->vshards > 1) {
+    for (uint32_t g = 0; g < h->vshards; ++g) {
+      vd_halo_plan_t p;
+      halo_plan(h->N, h->vshards, g, k, p);
+      Shard& sh = h->shards[g];
+      if (p.recv_top_rank >= 0)
+        CK(cudaMemcpyAsync(sh.top, h->shards[p.recv_top_rank].buf[h->cur] + (size_t)(sh.rows - p.halo_rows) * h->pitch,
+                           p.halo_rows * row_bytes, cudaMemcpyDeviceToDevice, h->stream));
+      if (p.recv_bot_rank >= 0)
+        CK(cudaMemcpyAsync(sh.bot, h->shards[p.recv_bot_rank].buf[h->cur], p.halo_rows * row_bytes,
+                           cudaMemcpyDeviceToDevice, h->stream));
+    }
+  }
+  for (auto& sh : h->shards) {
+    vd_status st = launch_pass(h, sh, k, may_empty);
+    if (st) return st;
+  }
+  h->cur ^= 1;
+  return VD_OK;
+}
+
+vd_status stamp_all(vd_ctx* h, const uint32_t* seeds) {
+  for (auto& sh : h->shards) {
+    vdk::stamp<<<grid_for((int64_t)h->s, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
+                                                                   (int)sh.rows, seeds, (int64_t)h->s);
+    vd_status st = after_launch(h, "stamp");
+    if (st) return st;
+  }
+  return VD_OK;
+}
+
+vd_status move_seeds(vd_ctx* h, const int16_t* disp_xy) {
+  vd_status st = upload_disp(h, disp_xy);
+  if (st) return st;
+  vdk::move_clamp<<<grid_for((int64_t)h->s, 256), 256, 0, h->stream>>>(h->seeds, h->disp, h->seeds_new,
+                                                                       (int64_t)h->s, (int)h->N);
+  return after_launch(h, "move_clamp");
+}
+
+vd_status reduce_to_host(vd_ctx* h, uint64_t* out) {
+  if (h->world > 1) {
+    CKN(g_nccl.AllReduce(h->counter, h->counter, 1, ncclUint64, ncclSum, h->comm, h->stream));
+  }
+  CK(cudaMemcpyAsync(h->counter_h, h->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  *out = *h->counter_h;
+  return VD_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int now;
+    if (prev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != prev) cudaSetDevice(prev);
+  }
+};
+
+void free_all(vd_ctx* h) {
+  for (auto& sh : h->shards) {
+    cudaFree(sh.buf[0]);
+    cudaFree(sh.buf[1]);
+    cudaFree(sh.top);
+    cudaFree(sh.bot);
+  }
+  h->shards.clear();
+  cudaFree(h->seeds);
+  cudaFree(h->seeds_new);
+  cudaFree(h->disp);
+  cudaFree(h->fwd);
+  cudaFree(h->counter);
+  if (h->disp_stage) cudaFreeHost(h->disp_stage);
+  if (h->counter_h) cudaFreeHost(h->counter_h);
+  if (h->disp_done) cudaEventDestroy(h->disp_done);
+  for (auto e : h->ev) cudaEventDestroy(e);
+  h->ev.clear();
+  if (h->comm && g_nccl.ok) g_nccl.CommDestroy(h->comm);
+  h->comm = nullptr;
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  h->stream = nullptr;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void vd_config_init(vd_config* cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof *cfg);
+  cfg->device = -1;
+  cfg->world = 1;
+}
+
+const char* vd_status_str(vd_status s) {
+  switch (s) {
+    case VD_OK: return "VD_OK";
+    case VD_ERR_ARG: return "VD_ERR_ARG";
+    case VD_ERR_RANGE: return "VD_ERR_RANGE";
+    case VD_ERR_STATE: return "VD_ERR_STATE";
+    case VD_ERR_CUDA: return "VD_ERR_CUDA";
+    case VD_ERR_NCCL: return "VD_ERR_NCCL";
+    case VD_ERR_OOM: return "VD_ERR_OOM";
+    default: return "VD_ERR_UNKNOWN";
+  }
+}
+
+const char* vd_last_error(vd_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+vd_status vd_nccl_unique_id(void* out128) {
+  if (!out128) return VD_ERR_ARG;
+  if (!nccl_load()) return VD_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return VD_ERR_NCCL;
+  memcpy(out128, &id, sizeof id);
+  return VD_OK;
+}
+
+vd_status vd_schedule_jfa(uint32_t N, uint32_t extras, uint32_t* ks, uint32_t cap, uint32_t* n) {
+  std::vector<uint32_t> v;
+  if (!ks || !n || schedule_jfa(N, extras, v) != 0 || v.size() > cap) return VD_ERR_ARG;
+  std::copy(v.begin(), v.end(), ks);
+  *n = (uint32_t)v.size();
+  return VD_OK;
+}
+
+vd_status vd_schedule_djfa(uint32_t N, uint64_t s, uint32_t d_max, uint32_t extras, uint32_t* ks, uint32_t cap,
+                           uint32_t* n) {
+  std::vector<uint32_t> v;
+  if (!ks || !n || schedule_djfa(N, s, d_max, extras, v) != 0 || v.size() > cap) return VD_ERR_ARG;
+  std::copy(v.begin(), v.end(), ks);
+  *n = (uint32_t)v.size();
+  return VD_OK;
+}
+
+vd_status vd_halo_plan(uint32_t N, uint32_t world, uint32_t rank, uint32_t k, vd_halo_plan_t* out) {
+  if (!out || world == 0 || rank >= world || k == 0 || N % world != 0) return VD_ERR_ARG;
+  halo_plan(N, world, rank, k, *out);
+  return VD_OK;
+}
+
+vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seeds_xy, const vd_config* cfg_in) {
+  if (!out) return VD_ERR_ARG;
+  *out = nullptr;
+  vd_config cfg;
+  vd_config_init(&cfg);
+  if (cfg_in) cfg = *cfg_in;
+  if (N < 2 || N > 65536 || s == 0 || s > (uint64_t)N * N || !seeds_xy) return VD_ERR_ARG;
+  if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) return VD_ERR_ARG;
+  const bool pow2 = (N & (N - 1)) == 0;
+  const uint32_t vsh = cfg.virtual_shards ? cfg.virtual_shards : 1;
+  const uint32_t G = cfg.world > 1 ? (uint32_t)cfg.world : vsh;
+  if (cfg.world > 1 && vsh > 1) return VD_ERR_ARG;
+  if (G > 1 && (!pow2 || N % G != 0 || (G & (G - 1)) != 0)) return VD_ERR_ARG;
+  if (cfg.world > 1 && !cfg.nccl_id) return VD_ERR_ARG;
+  for (int i = 0; i < 6; ++i)
+    if (cfg.reserved[i]) return VD_ERR_ARG;
+
+  // Validate and pack the seeds on the host (R-1, R-4).
+  std::vector<uint16_t> hxy;
+  const uint16_t* xy = seeds_xy;
+  if (is_device_ptr(seeds_xy)) {
+    hxy.resize(2 * s);
+    if (cudaMemcpy(hxy.data(), seeds_xy, 4 * s, cudaMemcpyDeviceToHost) != cudaSuccess) return VD_ERR_CUDA;
+    xy = hxy.data();
+  }
+  std::vector<uint32_t> packed(s);
+  for (uint64_t i = 0; i < s; ++i) {
+    const uint32_t x = xy[2 * i], y = xy[2 * i + 1];
+    if (x >= N || y >= N) return VD_ERR_RANGE;
+    if (N == 65536 && x == 65535 && y == 65535) return VD_ERR_RANGE;
+    packed[i] = (y << 16) | x;
+  }
+
+  vd_ctx* h = new vd_ctx();
+  h->N = N;
+  h->s = s;
+  h->pitch = ((int64_t)N + 31) / 32 * 32;
+  h->rank = cfg.rank;
+  h->world = cfg.world;
+  h->vshards = cfg.world > 1 ? 1 : vsh;
+  h->extras = cfg.extra_passes;
+  if (cfg.device >= 0) h->device = cfg.device;
+  else if (cudaGetDevice(&h->device) != cudaSuccess) { delete h; return VD_ERR_CUDA; }
+  DeviceGuard guard(h->device);
+
+  auto bail = [&](vd_status st) {
+    free_all(h);
+    delete h;
+    return st;
+  };
+#define CKC(expr)                                                                        \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess) return bail(e_ == cudaErrorMemoryAllocation ? VD_ERR_OOM : VD_ERR_CUDA); \
+  } while (0)
+
+  if (cfg.stream) h->stream = (cudaStream_t)cfg.stream;
+  else {
+    CKC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  // Bands: one per rank (world > 1) or `vshards` inside this handle.
+  const uint32_t B = N / G;
+  const uint32_t k1 = 1u << (ceil_log2_u64(N) - 1);
+  h->hcap = G > 1 ? std::min(k1, B) : 0;
+  const uint32_t nloc = cfg.world > 1 ? 1 : h->vshards;
+  for (uint32_t g = 0; g < nloc; ++g) {
+    Shard sh;
+    const uint32_t band = cfg.world > 1 ? (uint32_t)cfg.rank : g;
+    sh.row0 = G > 1 ? band * B : 0;
+    sh.rows = G > 1 ? B : N;
+    h->shards.push_back(sh);
+    Shard& r = h->shards.back();
+    const size_t bytes = (size_t)r.rows * h->pitch * sizeof(uint32_t);
+    CKC(cudaMalloc(&r.buf[0], bytes));
+    CKC(cudaMalloc(&r.buf[1], bytes));
+    CKC(cudaMemsetAsync(r.buf[0], 0xFF, bytes, h->stream));
+    CKC(cudaMemsetAsync(r.buf[1], 0xFF, bytes, h->stream));
+    if (h->hcap) {
+      const size_t hb = (size_t)h->hcap * h->pitch * sizeof(uint32_t);
+      CKC(cudaMalloc(&r.top, hb));
+      CKC(cudaMalloc(&r.bot, hb));
+      CKC(cudaMemsetAsync(r.top, 0xFF, hb, h->stream));
+      CKC(cudaMemsetAsync(r.bot, 0xFF, hb, h->stream));
+    }
+  }
+  CKC(cudaMalloc(&h->seeds, s * sizeof(uint32_t)));
+  CKC(cudaMalloc(&h->seeds_new, s * sizeof(uint32_t)));
+  CKC(cudaMalloc(&h->disp, s * sizeof(short2)));
+  CKC(cudaMallocHost(&h->disp_stage, s * sizeof(short2)));
+  CKC(cudaMalloc(&h->counter, sizeof(unsigned long long)));
+  CKC(cudaMallocHost(&h->counter_h, sizeof(unsigned long long)));
+  CKC(cudaEventCreateWithFlags(&h->disp_done, cudaEventDisableTiming));
+  CKC(cudaEventRecord(h->disp_done, h->stream));
+  CKC(cudaMemcpyAsync(h->seeds, packed.data(), s * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
+  CKC(cudaStreamSynchronize(h->stream));
+  if (cfg.world > 1) {
+    if (!nccl_load()) return bail(VD_ERR_NCCL);
+    ncclUniqueId id;
+    memcpy(&id, cfg.nccl_id, sizeof id);
+    if (g_nccl.CommInitRank(&h->comm, cfg.world, id, cfg.rank) != ncclSuccess) return bail(VD_ERR_NCCL);
+  }
+#undef CKC
+  *out = h;
+  return VD_OK;
+}
+
+void vd_destroy(vd_handle h) {
+  if (!h) return;
+  DeviceGuard guard(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  free_all(h);
+  delete h;
+}
+
+vd_status vd_jfa(vd_handle h) {
+  CHECK_HANDLE(h);
+  DeviceGuard guard(h->device);
+  std::vector<uint32_t> ks;
+  schedule_jfa(h->N, h->extras, ks);
+  for (auto& sh : h->shards) {  // JFA init: all EMPTY ...
+    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
+    vdk::fill_empty<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4);
+    vd_status st = after_launch(h, "fill_empty");
+    if (st) return st;
+  }
+  vd_status st = stamp_all(h, h->seeds);  // ... then each seed pixel holds its own label
+  if (st) return st;
+  // EMPTY can survive until the diagram is complete; the fast kernel's EMPTY variant
+  // is used for every JFA pass (it is exact either way).
+  for (uint32_t k : ks) {
+    st = run_pass(h, k, true);
+    if (st) return st;
+  }
+  h->last_passes = (uint32_t)ks.size();
+  h->has_diagram = true;
+  return VD_OK;
+}
+
+vd_status vd_move_seeds(vd_handle h, const int16_t* disp_xy) {
+  CHECK_HANDLE(h);
+  if (!disp_xy) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  vd_status st = move_seeds(h, disp_xy);
+  if (st) return st;
+  std::swap(h->seeds, h->seeds_new);
+  h->has_diagram = false;  // the diagram no longer matches the seeds
+  return VD_OK;
+}
+
+vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
+  CHECK_HANDLE(h);
+  if (!disp_xy) return VD_ERR_ARG;
+  if (!h->has_diagram) return fail(h, VD_ERR_STATE, "vd_djfa_step needs a diagram: call vd_jfa first");
+  DeviceGuard guard(h->device);
+  if (!h->fwd) CK(cudaMalloc(&h->fwd, (size_t)h->N * h->N * sizeof(uint32_t)));
+  std::vector<uint32_t> ks;
+  schedule_djfa(h->N, h->s, d_max, h->extras, ks);
+  // 1. SimulateParticles
+  vd_status st = move_seeds(h, disp_xy);
+  if (st) return st;
+  // 2. forward map old -> new (R-9)
+  const int gs = grid_for((int64_t)h->s, 256);
+  vdk::fwd_clear<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, (int64_t)h->s);
+  if ((st = after_launch(h, "fwd_clear"))) return st;
+  vdk::fwd_min<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, h->seeds_new, (int64_t)h->s);
+  if ((st = after_launch(h, "fwd_min"))) return st;
+  // 3. labels follow their seeds (reuse of VD_{t-1})
+  for (auto& sh : h->shards) {
+    const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
+    vdk::remap<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd);
+    if ((st = after_launch(h, "remap"))) return st;
+  }
+  // 4. re-stamp the new seed pixels
+  std::swap(h->seeds, h->seeds_new);
+  if ((st = stamp_all(h, h->seeds))) return st;
+  // 5. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
+  //    seed), so no EMPTY exists.
+  for (uint32_t k : ks) {
+    st = run_pass(h, k, false);
+    if (st) return st;
+  }
+  h->last_passes = (uint32_t)ks.size();
+  return VD_OK;
+}
+
+vd_status vd_set_labels(vd_handle h, const uint32_t* labels) {
+  CHECK_HANDLE(h);
+  if (!labels) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  uint64_t rows_total = 0;
+  for (auto& sh : h->shards) rows_total += sh.rows;
+  const uint64_t n = rows_total * h->N;
+  bool any_empty = false;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t c = labels[i];
+    if (c == VD_EMPTY) { any_empty = true; continue; }
+    if ((c & 0xFFFFu) >= h->N || (c >> 16) >= h->N) return fail(h, VD_ERR_RANGE, "label %u outside the grid", c);
+  }
+  size_t off_rows = 0;
+  for (auto& sh : h->shards) {
+    CK(cudaMemcpy2DAsync(sh.buf[h->cur], h->pitch * sizeof(uint32_t), labels + off_rows * h->N,
+                         h->N * sizeof(uint32_t), h->N * sizeof(uint32_t), sh.rows, cudaMemcpyHostToDevice, h->stream));
+    off_rows += sh.rows;
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  h->has_diagram = !any_empty;
+  return VD_OK;
+}
+
+vd_status vd_pass(vd_handle h, uint32_t k) {
+  CHECK_HANDLE(h);
+  if (k == 0 || k >= 65536) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  if (h->world > 1 || h->vshards > 1) {
+    const uint32_t G = h->world > 1 ? (uint32_t)h->world : h->vshards;
+    const uint32_t B = h->N / G;
+    if (k > B && k % B != 0) return fail(h, VD_ERR_ARG, "sharded pass needs k < band rows or a multiple of them");
+    if (k > h->hcap && k < B) return fail(h, VD_ERR_ARG, "halo capacity exceeded");
+  }
+  return run_pass(h, k, true);
+}
+
+vd_status vd_similarity(vd_handle h, vd_handle ref, double* pct, uint64_t* matches) {
+  CHECK_HANDLE(h);
+  CHECK_HANDLE(ref);
+  if (!pct && !matches) return VD_ERR_ARG;
+  if (ref->N != h->N || ref->world != h->world || ref->rank != h->rank || ref->vshards != h->vshards ||
+      ref->device != h->device)
+    return fail(h, VD_ERR_ARG, "vd_similarity: handles differ in N, sharding or device");
+  DeviceGuard guard(h->device);
+  if (ref->stream != h->stream) CK(cudaStreamSynchronize(ref->stream));
+  CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+  for (size_t g = 0; g < h->shards.size(); ++g) {
+    const Shard& a = h->shards[g];
+    const Shard& b = ref->shards[g];
+    const int64_t work = (int64_t)a.rows * ((h->N + 3) / 4);
+    vdk::match_count<<<grid_for(work, 256), 256, 0, h->stream>>>(a.buf[h->cur], b.buf[ref->cur], h->pitch,
+                                                                (int)a.rows, (int)h->N, h->counter);
+    vd_status st = after_launch(h, "match_count");
+    if (st) return st;
+  }
+  uint64_t m = 0;
+  vd_status st = reduce_to_host(h, &m);
+  if (st) return st;
+  if (matches) *matches = m;
+  if (pct) *pct = 100.0 * (double)m / ((double)h->N * (double)h->N);
+  return VD_OK;
+}
+
+vd_status vd_similarity_host(vd_handle h, const uint32_t* ref_labels, double* pct, uint64_t* matches) {
+  CHECK_HANDLE(h);
+  if (!ref_labels || (!pct && !matches)) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+  size_t off_rows = 0;
+  for (auto& sh : h->shards) {
+    // the idle ping-pong buffer is scratch between calls
+    uint32_t* scratch = sh.buf[h->cur ^ 1];
+    CK(cudaMemcpy2DAsync(scratch, h->pitch * sizeof(uint32_t), ref_labels + off_rows * h->N, h->N * sizeof(uint32_t),
+                         h->N * sizeof(uint32_t), sh.rows, cudaMemcpyDefault, h->stream));
+    const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
+    vdk::match_count<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], scratch, h->pitch, (int)sh.rows,
+                                                                (int)h->N, h->counter);
+    vd_status st = after_launch(h, "match_count");
+    if (st) return st;
+    off_rows += sh.rows;
+  }
+  uint64_t m = 0;
+  vd_status st = reduce_to_host(h, &m);
+  if (st) return st;
+  if (matches) *matches = m;
+  if (pct) *pct = 100.0 * (double)m / ((double)h->N * (double)h->N);
+  return VD_OK;
+}
+
+vd_status vd_label_hash(vd_handle h, uint64_t* out) {
+  CHECK_HANDLE(h);
+  if (!out) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+  for (auto& sh : h->shards) {
+    const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
+    vdk::label_hash<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
+                                                               (int)sh.rows, (int)h->N, h->counter);
+    vd_status st = after_launch(h, "label_hash");
+    if (st) return st;
+  }
+  return reduce_to_host(h, out);
+}
+
+vd_status vd_get_labels(vd_handle h, uint32_t* out) {
+  CHECK_HANDLE(h);
+  if (!out) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  size_t off_rows = 0;
+  for (auto& sh : h->shards) {
+    CK(cudaMemcpy2DAsync(out + off_rows * h->N, h->N * sizeof(uint32_t), sh.buf[h->cur], h->pitch * sizeof(uint32_t),
+                         h->N * sizeof(uint32_t), sh.rows, cudaMemcpyDeviceToHost, h->stream));
+    off_rows += sh.rows;
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  return VD_OK;
+}
+
+vd_status vd_get_seeds(vd_handle h, uint16_t* out_xy) {
+  CHECK_HANDLE(h);
+  if (!out_xy) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  std::vector<uint32_t> p(h->s);
+  CK(cudaMemcpyAsync(p.data(), h->seeds, h->s * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  for (uint64_t i = 0; i < h->s; ++i) {
+    out_xy[2 * i] = (uint16_t)(p[i] & 0xFFFFu);
+    out_xy[2 * i + 1] = (uint16_t)(p[i] >> 16);
+  }
+  return VD_OK;
+}
+
+vd_status vd_band(vd_handle h, uint32_t* row0, uint32_t* rows) {
+  if (!h || !row0 || !rows) return VD_ERR_ARG;
+  if (h->world > 1) {
+    *row0 = h->shards[0].row0;
+    *rows = h->shards[0].rows;
+  } else {
+    *row0 = 0;
+    *rows = h->N;
+  }
+  return VD_OK;
+}
+
+vd_status vd_last_passes(vd_handle h, uint32_t* passes) {
+  if (!h || !passes) return VD_ERR_ARG;
+  *passes = h->last_passes;
+  return VD_OK;
+}
+
+vd_status vd_synchronize(vd_handle h) {
+  CHECK_HANDLE(h);
+  DeviceGuard guard(h->device);
+  CK(cudaStreamSynchronize(h->stream));
+  return VD_OK;
+}
+
+vd_status vd_set_pass_timing(vd_handle h, int enable) {
+  CHECK_HANDLE(h);
+  h->timing = enable != 0;
+  return VD_OK;
+}
+
+vd_status vd_pass_timing(vd_handle h, double* ms, uint64_t* launches, uint64_t* pixels) {
+  CHECK_HANDLE(h);
+  DeviceGuard guard(h->device);
+  CK(cudaStreamSynchronize(h->stream));
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]));
+    total += t;
+  }
+  if (ms) *ms = total;
+  if (launches) *launches = h->timed_launches;
+  if (pixels) *pixels = h->timed_px;
+  h->ev_used = 0;
+  h->timed_launches = 0;
+  h->timed_px = 0;
+  return VD_OK;
+}
+
+vd_status vd_launch_count(vd_handle h, uint64_t* n) {
+  if (!h || !n) return VD_ERR_ARG;
+  *n = h->launches;
+  return VD_OK;
+}
+
+}  // extern "C"

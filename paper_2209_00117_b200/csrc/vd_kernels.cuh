@@ -1,0 +1,395 @@
+// vd_kernels.cuh -- sm_100a kernels of the dJFA hot path (arXiv 2209.00117).
+//
+// "P:n" = line n of the paper's LaTeX source; "R-n" = reading n in DESIGN.md §3.
+// Independent of oracle/: nothing here is shared with, or derived from, the CPU oracle.
+//
+// Label: uint32 (y << 16) | x of the claimed seed (R-1); EMPTY = 0xFFFFFFFF (R-4).
+// Diagram rows are padded to `pitch` labels (a multiple of 32 -> 128-B aligned rows), so
+// every thread moves 4 labels with one 128-bit load / store.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vdk {
+
+constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+constexpr int kThreads = 128;  // threads per CTA in the pass kernels (4 px each -> 512 columns)
+constexpr int kWalk = 16;      // output rows per thread in the column walk of the jump pass
+
+// ------------------------------------------------------------------ arguments
+
+// One jump pass over a band of rows [row0, row0 + rows) of the N x N grid.
+// Global row r of the INPUT diagram lives in
+//   in  + (r - row0)     * pitch   if row0 <= r < row0 + rows      (own band)
+//   top + (r - top_row0) * pitch   if r < row0                     (halo from rank above)
+//   bot + (r - bot_row0) * pitch   if r >= row0 + rows             (halo from rank below)
+// (vd.h vd_halo_plan).  With one band (row0 = 0, rows = N) the halos are never touched.
+struct PassArgs {
+  const uint32_t* __restrict__ in;
+  const uint32_t* __restrict__ top;
+  const uint32_t* __restrict__ bot;
+  uint32_t* __restrict__ out;
+  int64_t pitch;
+  int32_t N, row0, rows, top_row0, bot_row0, k;
+  int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / kWalk)
+  int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
+  uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
+  uint32_t sh16;    // 65536 (a run-time value on purpose)
+};
+
+__device__ __forceinline__ const uint32_t* row_ptr(const PassArgs& a, int r) {
+  if (r >= a.row0 && r < a.row0 + a.rows) return a.in + (int64_t)(r - a.row0) * a.pitch;
+  if (r < a.row0) return a.top + (int64_t)(r - a.top_row0) * a.pitch;
+  return a.bot + (int64_t)(r - a.bot_row0) * a.pitch;
+}
+
+__device__ __forceinline__ uint4 ld4(const uint32_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+__device__ __forceinline__ uint32_t get(const uint4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+// ------------------------------------------------------------------ fast jump pass
+//
+// out[p] = argmin over c in {in[p]} U {in[p + o*k] : o in Table 1, p + o*k in
+// the grid} of key(p, c) = (d2(p, c), c) lexicographically ("the distance function
+// is used as a criterion to check which flood carries the closest seed"; R-2, R-3, R-11).
+//
+// Shape (B200-first, not the paper's one-thread-per-pixel launch of P:204):
+//  * a thread owns 4 adjacent columns x..x+3 (one 128-bit load/store per row) and walks
+//    down its residue class y, y+k, y+2k, ... for kWalk output rows, keeping the three
+//    input rows y-k, y, y+k in registers: each step loads ONE new row (3 x LDG.128: the
+//    columns x-k, x, x+k), so every input label is fetched once per thread and serves
+//    the three outputs above/at/below it;
+//  * per label, dx^2 to its output column is computed once when the row is loaded and
+//    reused by the three outputs (dy differs);
+//  * CTAs are ordered x-fastest, then consecutive walk segments of one residue class, so
+//    the x +- k neighbours of a row are fetched by CTAs running at the same time (L2 hits)
+//    and DRAM sees each input label about once (8 B per pixel per pass + (kWalk+2)/kWalk).
+//  * Out-of-grid neighbours are replaced by a label that is already a candidate (the
+//    pixel's own column in the same row, or the centre row): a duplicate candidate cannot
+//    change a minimum, so no per-candidate validity test is needed.
+//  * Integer pipes: the per-pixel work is ~9 x (dy, d2, tie) + 2 nine-way minima, all
+//    exact 32-bit integer ops.  Distances run on the FMA pipe (IMAD, IMAD.HI), the
+//    tie-break and minima on the ALU pipe (VIADDMNMX, VIMNMX3), so both pipes share the
+//    load:  dx<<16 = IMAD(c, 2^16, -x<<16) (exact while |dx| < 2^15), dx^2 = mulhi(D, D);
+//    dy = mad.hi(c, 2^16, -y) = (c >> 16) - y; d2 = IMAD(dy, dy, dx^2).
+//  * Tie-break without 64-bit compares ("resolve later"): m = min_i d2_i, then
+//    out = min_i max(c_i, m - d2_i) in uint32.  For d2_i = m the term is c_i; for
+//    d2_i > m, m - d2_i wraps to >= 2^31, above every label in use (< 2^31).
+//    Requires N <= 32768 (so d2 < 2^31 and y < 2^15).
+//  * MAY_EMPTY (JFA passes): EMPTY is first mapped to the virtual label vempty =
+//    (C << 16) | C, C = 2N - 1 <= 32767: a point farther from every pixel than any real
+//    seed (min d2 = 2 N^2 > 2 (N-1)^2), still a label < 2^31 above every real label, and
+//    mapped back to EMPTY on store.  Requires N <= 16384.
+struct Row {
+  uint32_t c[12];   // labels: [0..3] column x+e-k, [4..7] x+e, [8..11] x+e+k (e = 0..3)
+  uint32_t dx2[12]; // (cx - (x+e))^2 for the matching output column x+e
+};
+
+__device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Load the three quads of one input row for output columns x..x+3: p points at (row, x);
+// the neighbour quads are at p + offL and p + offR (offsets fixed per thread, see
+// jump_pass_fast).  FIX: per-element substitution of out-of-grid columns, only for the
+// few CTAs that touch a grid edge where a quad is partly outside (k < 4, or N % 4 != 0).
+template <int KM, bool MAY_EMPTY, bool FIX>
+__device__ __forceinline__ void load_row(const uint32_t* __restrict__ p, int offL, int offR, int x, int k, int N,
+                                         uint32_t vempty, uint32_t sh16, const int (&xs16)[4], Row& R) {
+  const uint4 Lv = ld4(p + offL), C = ld4(p), Rv = ld4(p + offR);
+  const uint32_t w[12] = {Lv.x, Lv.y, Lv.z, Lv.w, C.x, C.y, C.z, C.w, Rv.x, Rv.y, Rv.z, Rv.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if constexpr (KM >= 4) { R.c[e] = w[e]; R.c[8 + e] = w[8 + e]; }
+    else { R.c[e] = w[4 + e - KM]; R.c[8 + e] = w[4 + e + KM]; }
+    R.c[4 + e] = w[4 + e];
+  }
+  if constexpr (FIX) {  // an out-of-grid column -> the pixel's own column (a duplicate)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (x + e - k < 0) R.c[e] = w[4 + e];
+      if (x + e + k >= N) R.c[8 + e] = w[4 + e];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    uint32_t c = R.c[i];
+    if (MAY_EMPTY) { c = __vminu2(c, vempty); R.c[i] = c; }  // EMPTY -> virtual far seed
+    const int D = (int)(c * sh16) + xs16[i & 3];              // (cx - (x+e)) << 16
+    R.dx2[i] = (uint32_t)__mulhi(D, D);                       // (cx - (x+e))^2
+  }
+}
+
+__device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const Row& Cn, int e,
+                                              uint32_t negy, uint32_t sh16) {
+  uint32_t c[9], d[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    c[j] = A.c[4 * j + e];  d[j] = A.dx2[4 * j + e];
+    c[3 + j] = B.c[4 * j + e];  d[3 + j] = B.dx2[4 * j + e];
+    c[6 + j] = Cn.c[4 * j + e]; d[6 + j] = Cn.dx2[4 * j + e];
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const int dy = (int)mad_hi_u32(c[i], sh16, negy);         // (c >> 16) - y
+    d[i] = (uint32_t)(dy * dy) + d[i];
+  }
+  const uint32_t m = __vimin3_u32(__vimin3_u32(d[0], d[1], d[2]), __vimin3_u32(d[3], d[4], d[5]),
+                                  __vimin3_u32(d[6], d[7], d[8]));
+  uint32_t w[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) w[i] = __viaddmax_u32(m, 0u - d[i], c[i]);  // max(m - d_i, c_i)
+  return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]),
+                      __vimin3_u32(w[6], w[7], w[8]));
+}
+
+// The walk of one thread (see the comment block above).  BANDED: the band has halo
+// buffers (multi-GPU or virtual shards); otherwise every input row inside the grid is in
+// `in` and the next row is one pointer increment away.
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX>
+__device__ __forceinline__ void walk(const PassArgs& a, int x, int y) {
+  const int k = a.k, N = a.N;
+  const int yend = a.row0 + a.rows;
+  // Neighbour quads.  k >= 4: the quads at x -+ k, replaced by the centre quad when outside
+  // the grid (then every element is a duplicate of the pixel's own column; exact when
+  // N % 4 == 0, else FIX repairs the last quad).  k < 4: the adjacent quads x -+ 4.
+  const int step4 = KM >= 4 ? k : 4;
+  const int offL = (x - step4 >= 0) ? -step4 : 0;
+  const int offR = (x + step4 < N) ? step4 : 0;
+  const uint32_t sh16 = a.sh16;  // 65536, from memory so ptxas keeps the multiplies on the FMA pipe
+  const int xs16[4] = {-(x << 16), -((x + 1) << 16), -((x + 2) << 16), -((x + 3) << 16)};
+
+  // Input rows outside the grid are replaced by the centre row (duplicates again).
+  const int64_t kp = (int64_t)k * a.pitch;
+  const uint32_t* pc = (BANDED ? row_ptr(a, y) : a.in + (int64_t)(y - a.row0) * a.pitch) + x;
+  const uint32_t* pp = (y - k >= 0) ? (BANDED ? row_ptr(a, y - k) + x : pc - kp) : pc;
+  Row r0, r1, r2;
+  load_row<KM, MAY_EMPTY, FIX>(pp, offL, offR, x, k, N, a.vempty, sh16, xs16, r0);
+  load_row<KM, MAY_EMPTY, FIX>(pc, offL, offR, x, k, N, a.vempty, sh16, xs16, r1);
+  uint32_t* po = a.out + (int64_t)(y - a.row0) * a.pitch + x;
+  // One output row: P = row y-k, C = row y, Nx <- row y+k (loaded here).  The three row
+  // registers rotate roles, so the loop body is unrolled by 3 and no row is copied.
+  int j = 0;
+  auto step = [&](const Row& P, const Row& C, Row& Nx) -> bool {
+    const int rn = y + k;
+    const uint32_t* pn;
+    if (BANDED) pn = rn < yend ? pc + kp : (rn >= N ? pc : row_ptr(a, rn) + x);
+    else pn = pc + (rn < N ? kp : 0);
+    load_row<KM, MAY_EMPTY, FIX>(pn, offL, offR, x, k, N, a.vempty, sh16, xs16, Nx);
+    const uint32_t negy = 0u - (uint32_t)y;
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t v = best_of_9(P, C, Nx, e, negy, sh16);
+      if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
+      o[e] = v;
+    }
+    *reinterpret_cast<uint4*>(po) = make_uint4(o[0], o[1], o[2], o[3]);
+    po += kp;
+    pc = pn;
+    y = rn;
+    return ++j < kWalk && y < yend;
+  };
+#pragma unroll 1
+  while (true) {
+    if (!step(r0, r1, r2)) break;
+    if (!step(r1, r2, r0)) break;
+    if (!step(r2, r0, r1)) break;
+  }
+}
+
+template <int KM, bool MAY_EMPTY, bool BANDED>
+__global__ void __launch_bounds__(kThreads, 4) jump_pass_fast(PassArgs a) {
+  const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
+  const int wk = (int)(blockIdx.x / (unsigned)a.xblocks);
+  const int res = wk / a.segs, seg = wk - res * a.segs;
+  const int x = (xb * kThreads + (int)threadIdx.x) * 4;
+  const int y = a.row0 + res + seg * kWalk * a.k;
+  if (x >= a.N || res >= a.k || y >= a.row0 + a.rows) return;
+  // Only CTAs at the left / right grid edge can hold a partly-outside quad.
+  const bool fix = (KM < 4 || (a.N & 3)) && (xb == 0 || xb == a.xblocks - 1);
+  if (fix) walk<KM, MAY_EMPTY, BANDED, true>(a, x, y);
+  else walk<KM, MAY_EMPTY, BANDED, false>(a, x, y);
+}
+
+// ------------------------------------------------------------------ wide jump pass
+//
+// Same pass for grids the fast kernel cannot take exactly (N > 32768, or EMPTY present
+// with N > 23170): uint64 squared distances, explicit EMPTY, lexicographic (d2, label).
+// One thread per 4 adjacent pixels of one row, nine 128-bit loads.
+__device__ __forceinline__ void consider_wide(uint32_t c, int x, int y, uint64_t& bd, uint32_t& bc) {
+  if (c == EMPTY) return;
+  int64_t dx = (int64_t)(c & 0xFFFFu) - x, dy = (int64_t)(c >> 16) - y;
+  uint64_t d = (uint64_t)(dx * dx) + (uint64_t)(dy * dy);
+  if (d < bd || (d == bd && c < bc)) { bd = d; bc = c; }
+}
+
+__global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
+  const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
+  const int yl = (int)(blockIdx.x / (unsigned)a.xblocks);
+  const int x = (xb * kThreads + (int)threadIdx.x) * 4;
+  if (x >= a.N || yl >= a.rows) return;
+  const int y = a.row0 + yl, k = a.k, N = a.N;
+  uint32_t best[4];
+  uint64_t bd[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { best[e] = EMPTY; bd[e] = ~0ull; }
+#pragma unroll
+  for (int oy = -1; oy <= 1; ++oy) {
+    int r = y + oy * k;
+    if (r < 0 || r >= N) continue;
+    const uint32_t* p = row_ptr(a, r);
+#pragma unroll
+    for (int ox = -1; ox <= 1; ++ox) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int q = x + e + ox * k;
+        if (x + e >= N || q < 0 || q >= N) continue;
+        consider_wide(p[q], x + e, y, bd[e], best[e]);
+      }
+    }
+  }
+  *reinterpret_cast<uint4*>(a.out + (int64_t)yl * a.pitch + x) = make_uint4(best[0], best[1], best[2], best[3]);
+}
+
+// ------------------------------------------------------------------ JFA init
+// P:68 "defining the positions as the starting points for each flood": every pixel
+// EMPTY, then each seed pixel holds its own label.
+__global__ void fill_empty(uint4* __restrict__ p, int64_t n4) {
+  const uint4 v = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// labels[seed pixel] <- seed label, for seeds whose row lies in [row0, row0 + rows).
+// Co-located seeds write the same value, so the unordered writes are benign.
+__global__ void stamp(uint32_t* __restrict__ g, int64_t pitch, int row0, int rows,
+                      const uint32_t* __restrict__ seeds, int64_t s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = seeds[i];
+    int y = (int)(c >> 16) - row0, x = (int)(c & 0xFFFFu);
+    if (y >= 0 && y < rows) g[(int64_t)y * pitch + x] = c;
+  }
+}
+
+// ------------------------------------------------------------------ dJFA
+// SimulateParticles (Alg. 1): new = clamp(old + disp) per axis (R-10); at
+// N = 65536 the EMPTY pixel (65535, 65535) is reserved -> (65534, 65535) (R-4).
+__global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __restrict__ disp,
+                           uint32_t* __restrict__ new_s, int64_t s, int N) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = old_s[i];
+    short2 d = disp[i];
+    int x = (int)(c & 0xFFFFu) + d.x, y = (int)(c >> 16) + d.y;
+    x = min(max(x, 0), N - 1);
+    y = min(max(y, 0), N - 1);
+    if (N == 65536 && x == 65535 && y == 65535) x = 65534;
+    new_s[i] = ((uint32_t)y << 16) | (uint32_t)x;
+  }
+}
+
+// Forward map (R-9): fwd[old_i] <- min over seeds j at the same old pixel of new_j.
+// Step 1 clears the entries at old seed pixels, step 2 takes the atomic minimum.
+__global__ void fwd_clear(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s, int64_t s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = old_s[i];
+    fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)] = EMPTY;
+  }
+}
+__global__ void fwd_min(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s,
+                        const uint32_t* __restrict__ new_s, int64_t s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = old_s[i];
+    atomicMin(&fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)], new_s[i]);
+  }
+}
+
+// Reuse VD_{t-1}: every label moves with its seed, labels[p] <- fwd[labels[p]].
+// Neighbouring pixels mostly share a label, so the gathers hit L1.
+__global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd) {
+  const int xq = (N + 3) / 4;
+  const int64_t total = (int64_t)rows * xq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / xq;
+    int x = (int)(i - r * xq) * 4;
+    uint4* p = reinterpret_cast<uint4*>(g + r * pitch + x);
+    uint4 v = *p;
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t c = w[e];
+      if (x + e < N && c != EMPTY) w[e] = __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu));
+    }
+    *p = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
+  __shared__ uint64_t part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) part[wid] = v;
+  __syncthreads();
+  uint64_t t = 0;
+  if (wid == 0) {
+    t = (lane < (int)(blockDim.x >> 5)) ? part[lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+// Eq. 5 numerator: count of pixels with equal labels in a band.
+__global__ void match_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t pitch,
+                            int rows, int N, unsigned long long* __restrict__ out) {
+  const int xq = (N + 3) / 4;
+  const int64_t total = (int64_t)rows * xq;
+  uint64_t cnt = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / xq;
+    int x = (int)(i - r * xq) * 4;
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(a + r * pitch + x));
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(b + r * pitch + x));
+    int nv = min(4, N - x);
+    cnt += (u.x == v.x) + (nv > 1 && u.y == v.y) + (nv > 2 && u.z == v.z) + (nv > 3 && u.w == v.w);
+  }
+  uint64_t t = block_sum_u64(cnt);
+  if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
+}
+
+__device__ __forceinline__ uint64_t smix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Checksum sum_p splitmix64((p << 32) | label[p]) over a band (p = global y*N + x).
+__global__ void label_hash(const uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N,
+                           unsigned long long* __restrict__ out) {
+  const int xq = (N + 3) / 4;
+  const int64_t total = (int64_t)rows * xq;
+  uint64_t h = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / xq;
+    int x = (int)(i - r * xq) * 4;
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(g + r * pitch + x));
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint64_t p = (uint64_t)(row0 + r) * (uint64_t)N + (uint64_t)x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (x + e < N) h += smix(((p + e) << 32) | w[e]);
+  }
+  uint64_t t = block_sum_u64(h);
+  if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)t);
+}
+
+}  // namespace vdk

@@ -1,0 +1,246 @@
+"""GPU parity: libvd (CUDA, through the C ABI) against the CPU oracle, bit-exact.
+
+Labels are integers, so the bar is element-by-element equality (north star: "GPU
+JFA/dJFA label maps must match the CPU JFA/dJFA bit-exactly on the same host-generated
+seeds and displacement streams").  Inputs: synth (seeded, shared by both sides).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+EMPTY = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def vd():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2209_00117_b200 as m
+    from paper_2209_00117_b200 import build
+    build.build()
+    m.load_library()
+    return m
+
+
+def _jfa_gpu(vd, N, xy, **cfg):
+    d = vd.VoronoiDiagram(N, xy, **cfg)
+    d.jfa()
+    return d
+
+
+SMALL = [(2, 1), (2, 3), (3, 2), (4, 2), (5, 3), (8, 5), (13, 7), (16, 16), (31, 9), (64, 16), (100, 40),
+         (127, 300), (128, 128), (257, 50), (1000, 50), (1024, 1024), (1031, 2000)]
+
+
+@pytest.mark.parametrize("N,s", SMALL)
+def test_jfa_bit_exact(vd, N, s):
+    xy = synth.uniform_seeds(N, s, rng_seed=N + s)
+    d = _jfa_gpu(vd, N, xy)
+    G = d.labels()
+    assert np.array_equal(G, oracle.jfa(N, xy))
+    assert d.last_passes() == len(oracle.jfa_schedule(N))
+
+
+@pytest.mark.parametrize("extras", [1, 2])
+def test_jfa_extras_bit_exact(vd, extras):
+    N, s = 200, 60
+    xy = synth.uniform_seeds(N, s, rng_seed=3)
+    d = _jfa_gpu(vd, N, xy, extra_passes=extras)
+    assert np.array_equal(d.labels(), oracle.jfa(N, xy, extras))
+
+
+@pytest.mark.parametrize("N", [2, 3, 5, 8, 13, 64, 100, 257, 1024])
+def test_single_pass_random_states_bit_exact(vd, N):
+    # One pass from arbitrary label maps (seeds and EMPTY mixed, not only reachable
+    # states), for every k regime: 1, 2, multiples of 4, >= 512 and non-powers of two
+    # (generic kernel).
+    rng = np.random.default_rng(N)
+    s = min(N * N, 40)
+    xy = synth.uniform_seeds(N, s, rng_seed=N)
+    labels = np.array([oracle.pack(int(xy[2 * i]), int(xy[2 * i + 1])) for i in range(s)] + [EMPTY], dtype=np.uint32)
+    d = vd.VoronoiDiagram(N, xy)
+    for trial in range(3):
+        G = labels[rng.integers(0, len(labels), size=(N, N))]
+        for k in sorted({1, 2, 3, 4, 5, 8, 16, 64, 512, 1024} | {max(1, N // 2)}):
+            d.set_labels(G)
+            d.jump_pass(k)
+            assert np.array_equal(d.labels(), oracle.jump_pass(G, k)), (trial, k)
+
+
+@pytest.mark.parametrize("case", ["one_seed_corner", "all_colocated", "corners", "every_pixel", "row", "diag"])
+def test_jfa_edge_cases(vd, case):
+    N = 37
+    if case == "one_seed_corner":
+        xy = np.array([N - 1, N - 1], dtype=np.uint16)
+    elif case == "all_colocated":
+        xy = np.array([5, 7] * 20, dtype=np.uint16)
+    elif case == "corners":
+        xy = np.array([0, 0, N - 1, 0, 0, N - 1, N - 1, N - 1], dtype=np.uint16)
+    elif case == "every_pixel":
+        yy, xx = np.mgrid[0:N, 0:N]
+        xy = np.stack([xx.ravel(), yy.ravel()], 1).astype(np.uint16).ravel()
+    elif case == "row":
+        xy = np.array([[x, 3] for x in range(0, N, 3)], dtype=np.uint16).ravel()
+    else:
+        xy = np.array([[i, i] for i in range(N)], dtype=np.uint16).ravel()
+    d = _jfa_gpu(vd, N, xy)
+    assert np.array_equal(d.labels(), oracle.jfa(N, xy))
+
+
+def _djfa_run(vd, N, s, dmax, frames, seed, **cfg):
+    xy = synth.uniform_seeds(N, s, rng_seed=seed)
+    d = _jfa_gpu(vd, N, xy, **cfg)
+    G = oracle.jfa(N, xy)
+    assert np.array_equal(d.labels(), G)
+    for f in range(frames):
+        disp = synth.displacements(s, dmax, f, rng_seed=seed)
+        d.djfa_step(disp, dmax)
+        G, xy, n = oracle.djfa_step(N, xy, disp, dmax, G)
+        assert d.last_passes() == n
+        assert np.array_equal(d.seeds(), xy), f
+        assert np.array_equal(d.labels(), G), f
+    return d, G, xy
+
+
+def test_djfa_c1_all_frames(vd):
+    # BASELINE.json configs[0]: 64x64, 16 uniform seeds, 10 dJFA time steps
+    _djfa_run(vd, 64, 16, 1, 10, 2209)
+
+
+@pytest.mark.parametrize("N,s,dmax", [(256, 256, 1), (256, 256, 4), (300, 100, 7), (1024, 1024, 1),
+                                      (1024, 4096, 64), (512, 2048, 300), (64, 4096, 2)])
+def test_djfa_bit_exact(vd, N, s, dmax):
+    _djfa_run(vd, N, s, dmax, 4, N * 7 + s)
+
+
+def test_djfa_c2_prefix(vd):
+    # BASELINE.json configs[1]: 1024x1024, 1024 seeds, +-1 px moves (first 20 of 100 steps)
+    _djfa_run(vd, 1024, 1024, 1, 20, 2209)
+
+
+def test_djfa_clamp_at_borders(vd):
+    # displacements far larger than the grid: every seed is clamped to an edge
+    N, s = 64, 40
+    xy = synth.uniform_seeds(N, s, rng_seed=1)
+    d = _jfa_gpu(vd, N, xy)
+    G = oracle.jfa(N, xy)
+    for f in range(3):
+        disp = synth.displacements(s, 200, f, rng_seed=1)
+        d.djfa_step(disp, 200)
+        G, xy, _ = oracle.djfa_step(N, xy, disp, 200, G)
+        assert np.array_equal(d.labels(), G)
+
+
+def test_djfa_device_displacements(vd):
+    N, s = 512, 512
+    xy = synth.uniform_seeds(N, s, rng_seed=4)
+    d = _jfa_gpu(vd, N, xy)
+    G = oracle.jfa(N, xy)
+    for f in range(3):
+        disp = synth.displacements(s, 3, f, rng_seed=4)
+        d.djfa_step(torch.from_numpy(disp).cuda(), 3)
+        G, xy, _ = oracle.djfa_step(N, xy, disp, 3, G)
+        assert np.array_equal(d.labels(), G)
+
+
+def test_djfa_before_jfa_is_state_error(vd):
+    d = vd.VoronoiDiagram(16, np.array([1, 1, 9, 9], dtype=np.uint16))
+    with pytest.raises(vd.VDError) as e:
+        d.djfa_step(np.zeros(4, dtype=np.int16), 1)
+    assert e.value.status == vd.VD_ERR_STATE
+    d.jfa()
+    d.move_seeds(np.array([1, 0, 0, 1], dtype=np.int16))  # diagram now stale
+    with pytest.raises(vd.VDError):
+        d.djfa_step(np.zeros(4, dtype=np.int16), 1)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_virtual_shards_bit_identical(vd, G):
+    # The row-band path (halo plan + banded kernel) on one GPU: identical to 1 band and to
+    # the oracle, for JFA (k up to N/2 >= band height) and dJFA.
+    N, s, dmax = 256, 200, 3
+    xy = synth.uniform_seeds(N, s, rng_seed=G)
+    one = _jfa_gpu(vd, N, xy)
+    many = _jfa_gpu(vd, N, xy, virtual_shards=G)
+    ref = oracle.jfa(N, xy)
+    assert np.array_equal(many.labels(), ref) and np.array_equal(one.labels(), ref)
+    assert many.label_hash() == one.label_hash() == oracle.label_hash(ref)
+    for f in range(3):
+        disp = synth.displacements(s, dmax, f, rng_seed=G)
+        one.djfa_step(disp, dmax)
+        many.djfa_step(disp, dmax)
+        ref, xy, _ = oracle.djfa_step(N, xy, disp, dmax, ref)
+        assert np.array_equal(many.labels(), ref), f
+        assert many.label_hash() == one.label_hash() == oracle.label_hash(ref)
+        assert many.match_count(many) == N * N
+
+
+def test_similarity_and_hash_match_oracle(vd):
+    N, s = 300, 77
+    xy = synth.uniform_seeds(N, s, rng_seed=12)
+    a = _jfa_gpu(vd, N, xy)
+    b = vd.VoronoiDiagram(N, xy)
+    b.jfa()
+    disp = synth.displacements(s, 5, 0, rng_seed=12)
+    b.djfa_step(disp, 5)
+    A, B = a.labels(), b.labels()
+    pct, m = vd.vd_similarity(a.h, b.h)
+    assert m == oracle.match_count(A, B)
+    assert pct == pytest.approx(100.0 * m / (N * N), abs=1e-12)
+    E = oracle.exact(N, xy)
+    pct_h, m_h = vd.vd_similarity_host(a.h, E)
+    assert m_h == oracle.match_count(A, E)
+    assert a.label_hash() == oracle.label_hash(A)
+    assert b.label_hash() == oracle.label_hash(B)
+
+
+def test_c3_full_size_bit_exact(vd):
+    # BASELINE.json configs[2]: 4096x4096, 65,536 seeds, +-1 px moves; JFA + 3 dJFA frames,
+    # every pixel compared.
+    _djfa_run(vd, 4096, 65536, 1, 3, 2209)
+
+
+def test_c3_move_radius_sweep_bit_exact(vd):
+    # configs[2]'s sweep over the move radius: the delta schedule grows with d_max
+    N, s = 4096, 65536
+    for dmax in (8, 64, 512):
+        d, G, xy = _djfa_run(vd, N, s, dmax, 1, 100 + dmax)
+        assert d.last_passes() == len(oracle.djfa_schedule(N, s, dmax))
+
+
+@pytest.mark.slow
+def test_c4_bench_config_full_grid(vd):
+    # BASELINE.json configs[3] at the size bench.py times (16384^2, 2^20 seeds, +-1 px), in
+    # the same launch configuration: JFA bootstrap + 2 dJFA frames, whole-diagram hash and
+    # match count against the oracle, plus properties that hold at any size.
+    N, s = 16384, 1 << 20
+    xy = synth.uniform_seeds(N, s, rng_seed=2209)
+    d = _jfa_gpu(vd, N, xy)
+    G = oracle.jfa(N, xy)
+    assert d.label_hash() == oracle.label_hash(G)
+    for f in range(2):
+        disp = synth.displacements(s, 1, f, rng_seed=2209)
+        d.djfa_step(disp, 1)
+        G, xy, _ = oracle.djfa_step(N, xy, disp, 1, G)
+        assert d.label_hash() == oracle.label_hash(G)
+        _, m = vd.vd_similarity_host(d.h, G)
+        assert m == N * N
+    # every seed pixel holds its own label
+    L = d.labels()
+    lx, ly = xy[0::2].astype(np.int64), xy[1::2].astype(np.int64)
+    assert np.array_equal(L[ly, lx], (ly.astype(np.uint32) << 16) | lx.astype(np.uint32))
+    # sampled pixels against the exact nearest seed (Eq. 1), computed one by one
+    rng = np.random.default_rng(0)
+    py, px = rng.integers(0, N, 400), rng.integers(0, N, 400)
+    good = 0
+    for y, x in zip(py, px):
+        d2 = (lx - x) ** 2 + (ly - y) ** 2
+        m = d2.min()
+        best = ((ly[d2 == m].astype(np.uint32) << 16) | lx[d2 == m].astype(np.uint32)).min()
+        good += int(L[y, x] == best)
+    assert good >= 396  # P:268 "nearly 100%"
