@@ -188,7 +188,10 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     vd.load_library()
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream shared by torch and libvd: events recorded on it bracket
+    # exactly the library's kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     def barrier():
         if world > 1:

@@ -29,7 +29,8 @@ __all__ = [
 
 EMPTY = 0xFFFFFFFF
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libvd.so")
+# VD_LIB overrides the library path (kernel-variant experiments in scripts/); default in-tree.
+_LIB_PATH = os.environ.get("VD_LIB") or os.path.join(_PKG, "libvd.so")
 _lib = None
 
 VD_OK, VD_ERR_ARG, VD_ERR_RANGE, VD_ERR_STATE, VD_ERR_CUDA, VD_ERR_NCCL, VD_ERR_OOM = 0, -1, -2, -3, -4, -5, -6

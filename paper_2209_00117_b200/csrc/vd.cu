@@ -238,6 +238,22 @@ vd_status timed_end(vd_ctx* h, uint64_t px) {
 }
 
 // Which kernel variant can take this pass exactly (see vd_kernels.cuh).
+// Opt every fast-pass instantiation into the largest staging size (vdk::pass_smem).
+cudaError_t set_smem_attrs() {
+  static cudaError_t done = cudaErrorNotReady;
+  if (done != cudaErrorNotReady) return done;
+  cudaError_t e = cudaSuccess;
+  const int bytes = vdk::kSmemBudget;  // pass_smem(k) <= kSmemBudget for every k
+#define VD_ATTR(KM, ME, BD) \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  VD_ATTR(1, true, true) VD_ATTR(1, true, false) VD_ATTR(1, false, true) VD_ATTR(1, false, false)
+  VD_ATTR(2, true, true) VD_ATTR(2, true, false) VD_ATTR(2, false, true) VD_ATTR(2, false, false)
+  VD_ATTR(4, true, true) VD_ATTR(4, true, false) VD_ATTR(4, false, true) VD_ATTR(4, false, false)
+#undef VD_ATTR
+  done = e;
+  return e;
+}
+
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
 
 vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
@@ -264,18 +280,21 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
   if (fast_ok(h->N, may_empty) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, B);
     const uint32_t per_res = (B + k - 1) / k;
-    a.segs = (int)((per_res + vdk::kWalk - 1) / vdk::kWalk);
+    a.walk = vdk::walk_len((int)k);
+    a.segs = (int)((per_res + a.walk - 1) / a.walk);
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
     const bool banded = sh.top != nullptr;
+    CK(set_smem_attrs());
+    const size_t sm = vdk::pass_smem((int)k);
 #define VD_LAUNCH(KM)                                                                        \
   do {                                                                                       \
     if (may_empty) {                                                                         \
-      if (banded) vdk::jump_pass_fast<KM, true, true><<<grid, blk, 0, h->stream>>>(a);      \
-      else vdk::jump_pass_fast<KM, true, false><<<grid, blk, 0, h->stream>>>(a);            \
+      if (banded) vdk::jump_pass_fast<KM, true, true><<<grid, blk, sm, h->stream>>>(a);     \
+      else vdk::jump_pass_fast<KM, true, false><<<grid, blk, sm, h->stream>>>(a);           \
     } else {                                                                                 \
-      if (banded) vdk::jump_pass_fast<KM, false, true><<<grid, blk, 0, h->stream>>>(a);     \
-      else vdk::jump_pass_fast<KM, false, false><<<grid, blk, 0, h->stream>>>(a);           \
+      if (banded) vdk::jump_pass_fast<KM, false, true><<<grid, blk, sm, h->stream>>>(a);    \
+      else vdk::jump_pass_fast<KM, false, false><<<grid, blk, sm, h->stream>>>(a);          \
     }                                                                                        \
   } while (0)
     if (k == 1) VD_LAUNCH(1);
@@ -284,6 +303,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
 #undef VD_LAUNCH
   } else {
     a.segs = 1;
+    a.walk = 1;
     const int64_t blocks = (int64_t)a.xblocks * B;
     vdk::jump_pass_wide<<<dim3((unsigned)blocks), dim3(vdk::kThreads), 0, h->stream>>>(a);
   }

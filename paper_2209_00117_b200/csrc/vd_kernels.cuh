@@ -14,7 +14,12 @@ namespace vdk {
 
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr int kThreads = 128;  // threads per CTA in the pass kernels (4 px each -> 512 columns)
-constexpr int kWalk = 16;      // output rows per thread in the column walk of the jump pass
+#ifndef VD_MIN_BLOCKS
+#define VD_MIN_BLOCKS 4        // CTAs per SM the register allocation must allow
+#endif
+#ifndef VD_DY_ALU
+#define VD_DY_ALU 1            // 1: dy on the ALU pipe (LEA.HI), 0: on the FMA pipe (IMAD.HI)
+#endif
 
 // ------------------------------------------------------------------ arguments
 
@@ -31,7 +36,8 @@ struct PassArgs {
   uint32_t* __restrict__ out;
   int64_t pitch;
   int32_t N, row0, rows, top_row0, bot_row0, k;
-  int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / kWalk)
+  int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / walk)
+  int32_t walk;     // output rows per walk (walk_len(k))
   int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
@@ -59,7 +65,7 @@ __device__ __forceinline__ uint32_t get(const uint4& v, int e) {
 //
 // Shape (B200-first, not the paper's one-thread-per-pixel launch of P:204):
 //  * a thread owns 4 adjacent columns x..x+3 (one 128-bit load/store per row) and walks
-//    down its residue class y, y+k, y+2k, ... for kWalk output rows, keeping the three
+//    down its residue class y, y+k, y+2k, ... for up to kMaxWalk output rows, keeping the three
 //    input rows y-k, y, y+k in registers: each step loads ONE new row (3 x LDG.128: the
 //    columns x-k, x, x+k), so every input label is fetched once per thread and serves
 //    the three outputs above/at/below it;
@@ -67,7 +73,7 @@ __device__ __forceinline__ uint32_t get(const uint4& v, int e) {
 //    reused by the three outputs (dy differs);
 //  * CTAs are ordered x-fastest, then consecutive walk segments of one residue class, so
 //    the x +- k neighbours of a row are fetched by CTAs running at the same time (L2 hits)
-//    and DRAM sees each input label about once (8 B per pixel per pass + (kWalk+2)/kWalk).
+//    and DRAM sees each input label about once (8 B per pixel per pass).
 //  * Out-of-grid neighbours are replaced by a label that is already a candidate (the
 //    pixel's own column in the same row, or the centre row): a duplicate candidate cannot
 //    change a minimum, so no per-candidate validity test is needed.
@@ -95,14 +101,59 @@ __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t 
   return d;
 }
 
-// Load the three quads of one input row for output columns x..x+3: p points at (row, x);
-// the neighbour quads are at p + offL and p + offR (offsets fixed per thread, see
-// jump_pass_fast).  FIX: per-element substitution of out-of-grid columns, only for the
-// few CTAs that touch a grid edge where a quad is partly outside (k < 4, or N % 4 != 0).
+// ---- shared-memory row staging with cp.async.bulk (TMA bulk copies) -----------------
+constexpr int kW = 4 * kThreads;         // columns per CTA
+constexpr int kMaxWalk = 16;             // output rows per walk (upper bound)
+constexpr int kSmemBudget = 48 * 1024;   // staged rows per CTA (4 CTAs per SM)
+
+// Elements of one staged input row: columns [x0 - K4, x0 + W + K4) when k < W (K4 = k
+// rounded up to 4), else three W-wide spans at x0 - k, x0, x0 + k.
+__host__ __device__ inline int stage_elems(int k) {
+  return k >= kW ? 3 * kW : kW + 2 * ((k + 3) & ~3);
+}
+// Output rows per walk so that walk + 2 staged rows fit the budget.
+__host__ __device__ inline int walk_len(int k) {
+  const int rows = kSmemBudget / (stage_elems(k) * 4 + 8);
+  return rows - 2 < 1 ? 1 : (rows - 2 > kMaxWalk ? kMaxWalk : rows - 2);
+}
+__host__ __device__ inline size_t pass_smem(int k) {
+  return (size_t)(walk_len(k) + 2) * (stage_elems(k) * 4 + 8);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Build one Row (labels + dx^2) for output columns x..x+3 from a staged input row.
+// li / ci / ri: element offsets of the left / centre / right quads in the stage.
 template <int KM, bool MAY_EMPTY, bool FIX>
-__device__ __forceinline__ void load_row(const uint32_t* __restrict__ p, int offL, int offR, int x, int k, int N,
-                                         uint32_t vempty, uint32_t sh16, const int (&xs16)[4], Row& R) {
-  const uint4 Lv = ld4(p + offL), C = ld4(p), Rv = ld4(p + offR);
+__device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, int li, int ci, int ri, int x, int k,
+                                              int N, uint32_t vempty, uint32_t sh16, const int (&xs16)[4], Row& R) {
+  const uint4 Lv = *reinterpret_cast<const uint4*>(st + li);
+  const uint4 C = *reinterpret_cast<const uint4*>(st + ci);
+  const uint4 Rv = *reinterpret_cast<const uint4*>(st + ri);
   const uint32_t w[12] = {Lv.x, Lv.y, Lv.z, Lv.w, C.x, C.y, C.z, C.w, Rv.x, Rv.y, Rv.z, Rv.w};
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -137,7 +188,11 @@ __device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const 
   }
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
-    const int dy = (int)mad_hi_u32(c[i], sh16, negy);         // (c >> 16) - y
+#if VD_DY_ALU
+    const int dy = (int)((c[i] >> 16) + negy);                 // (c >> 16) - y  (LEA.HI, ALU pipe)
+#else
+    const int dy = (int)mad_hi_u32(c[i], sh16, negy);         // (c >> 16) - y  (IMAD.HI, FMA pipe)
+#endif
     d[i] = (uint32_t)(dy * dy) + d[i];
   }
   const uint32_t m = __vimin3_u32(__vimin3_u32(d[0], d[1], d[2]), __vimin3_u32(d[3], d[4], d[5]),
@@ -149,39 +204,80 @@ __device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const 
                       __vimin3_u32(w[6], w[7], w[8]));
 }
 
-// The walk of one thread (see the comment block above).  BANDED: the band has halo
-// buffers (multi-GPU or virtual shards); otherwise every input row inside the grid is in
-// `in` and the next row is one pointer increment away.
+// One CTA = 512 columns x one walk (up to kMaxWalk output rows of one residue class
+// y0, y0+k, ...).  At entry, thread 0 stages ALL of the walk's input rows
+// y0-k, y0, ..., y_last+k into shared memory with cp.async.bulk, one mbarrier per row;
+// the threads then consume the rows in order as they land -- no ring, no refills, no block
+// barriers in the loop.  Every thread turns a staged row into registers (Row) once and the
+// three row registers rotate as in a column walk.  Rows outside the grid are replaced by
+// the centre row (the producer stages that row again), columns outside the grid by the
+// pixel's own column: duplicates never change a minimum.
+// BANDED: rows beyond the band come from the halo buffers (row_ptr).
 template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX>
-__device__ __forceinline__ void walk(const PassArgs& a, int x, int y) {
+__device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t* smem) {
   const int k = a.k, N = a.N;
+  const int tid = (int)threadIdx.x;
+  const int x = x0 + 4 * tid;
   const int yend = a.row0 + a.rows;
-  // Neighbour quads.  k >= 4: the quads at x -+ k, replaced by the centre quad when outside
-  // the grid (then every element is a duplicate of the pixel's own column; exact when
-  // N % 4 == 0, else FIX repairs the last quad).  k < 4: the adjacent quads x -+ 4.
+  const int nout = min(a.walk, (yend - y0 + k - 1) / k);  // output rows of this walk
+  const int nlist = nout + 2;                              // staged input rows
+  const bool spans3 = k >= kW;
+  const int K4 = (k + 3) & ~3;
+  const int SE = stage_elems(k);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
+
+  if (tid == 0) {
+    for (int i = 0; i < nlist; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int P = (int)a.pitch;
+    for (int i = 0; i < nlist; ++i) {
+      int r = y0 + (i - 1) * k;
+      if (r < 0) r += k;
+      else if (r >= N) r -= k;
+      const uint32_t* src = BANDED ? row_ptr(a, r) : a.in + (int64_t)(r - a.row0) * a.pitch;
+      uint32_t* dst = smem + (size_t)i * SE;
+      if (!spans3) {
+        const int base = x0 - K4;
+        const int lo = max(base, 0), hi = min(x0 + kW + K4, P);
+        mbar_expect_tx(&bars[i], (uint32_t)(hi - lo) * 4u);
+        bulk_g2s(dst + (lo - base), src + lo, (uint32_t)(hi - lo) * 4u, &bars[i]);
+      } else {
+        const int lL = max(x0 - k, 0), hL = min(x0 - k + kW, P);
+        const int lC = x0, hC = min(x0 + kW, P);
+        const int lR = max(x0 + k, 0), hR = min(x0 + k + kW, P);
+        mbar_expect_tx(&bars[i], 4u * (uint32_t)(max(hL - lL, 0) + (hC - lC) + max(hR - lR, 0)));
+        if (lL < hL) bulk_g2s(dst + (lL - (x0 - k)), src + lL, (uint32_t)(hL - lL) * 4u, &bars[i]);
+        bulk_g2s(dst + kW, src + lC, (uint32_t)(hC - lC) * 4u, &bars[i]);
+        if (lR < hR) bulk_g2s(dst + 2 * kW + (lR - (x0 + k)), src + lR, (uint32_t)(hR - lR) * 4u, &bars[i]);
+      }
+    }
+  }
+  __syncthreads();  // barrier initialisation visible to every thread
+
+  // quad offsets in a stage (out-of-grid neighbour quads -> the centre quad)
   const int step4 = KM >= 4 ? k : 4;
-  const int offL = (x - step4 >= 0) ? -step4 : 0;
-  const int offR = (x + step4 < N) ? step4 : 0;
+  const int ci = spans3 ? kW + 4 * tid : K4 + 4 * tid;
+  const int li = (x - step4 >= 0) ? (spans3 ? 4 * tid : ci - step4) : ci;
+  const int ri = (x + step4 < N) ? (spans3 ? 2 * kW + 4 * tid : ci + step4) : ci;
   const uint32_t sh16 = a.sh16;  // 65536, from memory so ptxas keeps the multiplies on the FMA pipe
   const int xs16[4] = {-(x << 16), -((x + 1) << 16), -((x + 2) << 16), -((x + 3) << 16)};
+  const bool active = x < N;
 
-  // Input rows outside the grid are replaced by the centre row (duplicates again).
-  const int64_t kp = (int64_t)k * a.pitch;
-  const uint32_t* pc = (BANDED ? row_ptr(a, y) : a.in + (int64_t)(y - a.row0) * a.pitch) + x;
-  const uint32_t* pp = (y - k >= 0) ? (BANDED ? row_ptr(a, y - k) + x : pc - kp) : pc;
+  auto consume = [&](int i, Row& R) {
+    mbar_wait(&bars[i], 0u);
+    row_from_smem<KM, MAY_EMPTY, FIX>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16, R);
+  };
+
   Row r0, r1, r2;
-  load_row<KM, MAY_EMPTY, FIX>(pp, offL, offR, x, k, N, a.vempty, sh16, xs16, r0);
-  load_row<KM, MAY_EMPTY, FIX>(pc, offL, offR, x, k, N, a.vempty, sh16, xs16, r1);
-  uint32_t* po = a.out + (int64_t)(y - a.row0) * a.pitch + x;
-  // One output row: P = row y-k, C = row y, Nx <- row y+k (loaded here).  The three row
-  // registers rotate roles, so the loop body is unrolled by 3 and no row is copied.
+  consume(0, r0);
+  consume(1, r1);
+  int y = y0;
+  uint32_t* po = a.out + (int64_t)(y0 - a.row0) * a.pitch + x;
+  const int64_t kp = (int64_t)k * a.pitch;
   int j = 0;
+  // Output row j: P = row j (y-k), C = row j+1 (y), Nx <- row j+2 (y+k).
   auto step = [&](const Row& P, const Row& C, Row& Nx) -> bool {
-    const int rn = y + k;
-    const uint32_t* pn;
-    if (BANDED) pn = rn < yend ? pc + kp : (rn >= N ? pc : row_ptr(a, rn) + x);
-    else pn = pc + (rn < N ? kp : 0);
-    load_row<KM, MAY_EMPTY, FIX>(pn, offL, offR, x, k, N, a.vempty, sh16, xs16, Nx);
+    consume(j + 2, Nx);
     const uint32_t negy = 0u - (uint32_t)y;
     uint32_t o[4];
 #pragma unroll
@@ -190,11 +286,10 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x, int y) {
       if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
       o[e] = v;
     }
-    *reinterpret_cast<uint4*>(po) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (active) *reinterpret_cast<uint4*>(po) = make_uint4(o[0], o[1], o[2], o[3]);
     po += kp;
-    pc = pn;
-    y = rn;
-    return ++j < kWalk && y < yend;
+    y += k;
+    return ++j < nout;
   };
 #pragma unroll 1
   while (true) {
@@ -205,17 +300,18 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x, int y) {
 }
 
 template <int KM, bool MAY_EMPTY, bool BANDED>
-__global__ void __launch_bounds__(kThreads, 4) jump_pass_fast(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
+  extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
   const int wk = (int)(blockIdx.x / (unsigned)a.xblocks);
   const int res = wk / a.segs, seg = wk - res * a.segs;
-  const int x = (xb * kThreads + (int)threadIdx.x) * 4;
-  const int y = a.row0 + res + seg * kWalk * a.k;
-  if (x >= a.N || res >= a.k || y >= a.row0 + a.rows) return;
+  const int x0 = xb * kW;
+  const int y0 = a.row0 + res + seg * a.walk * a.k;
+  if (res >= a.k || y0 >= a.row0 + a.rows) return;  // uniform over the CTA
   // Only CTAs at the left / right grid edge can hold a partly-outside quad.
   const bool fix = (KM < 4 || (a.N & 3)) && (xb == 0 || xb == a.xblocks - 1);
-  if (fix) walk<KM, MAY_EMPTY, BANDED, true>(a, x, y);
-  else walk<KM, MAY_EMPTY, BANDED, false>(a, x, y);
+  if (fix) walk<KM, MAY_EMPTY, BANDED, true>(a, x0, y0, dyn_smem);
+  else walk<KM, MAY_EMPTY, BANDED, false>(a, x0, y0, dyn_smem);
 }
 
 // ------------------------------------------------------------------ wide jump pass
