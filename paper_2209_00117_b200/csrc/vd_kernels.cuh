@@ -103,8 +103,14 @@ __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t 
 
 // ---- shared-memory row staging with cp.async.bulk (TMA bulk copies) -----------------
 constexpr int kW = 4 * kThreads;         // columns per CTA
-constexpr int kMaxWalk = 16;             // output rows per walk (upper bound)
-constexpr int kSmemBudget = 48 * 1024;   // staged rows per CTA (4 CTAs per SM)
+#ifndef VD_MAX_WALK
+#define VD_MAX_WALK 16
+#endif
+#ifndef VD_SMEM_KB
+#define VD_SMEM_KB 48
+#endif
+constexpr int kMaxWalk = VD_MAX_WALK;    // output rows per walk (upper bound)
+constexpr int kSmemBudget = VD_SMEM_KB * 1024;  // staged rows per CTA
 
 // Elements of one staged input row: columns [x0 - K4, x0 + W + K4) when k < W (K4 = k
 // rounded up to 4), else three W-wide spans at x0 - k, x0, x0 + k.
@@ -226,9 +232,10 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   const int SE = stage_elems(k);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
 
+  if (tid < nlist) mbar_init(&bars[tid], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();  // barrier initialisation visible to every thread (and to the async proxy)
   if (tid == 0) {
-    for (int i = 0; i < nlist; ++i) mbar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const int P = (int)a.pitch;
     for (int i = 0; i < nlist; ++i) {
       int r = y0 + (i - 1) * k;
@@ -252,7 +259,6 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
       }
     }
   }
-  __syncthreads();  // barrier initialisation visible to every thread
 
   // quad offsets in a stage (out-of-grid neighbour quads -> the centre quad)
   const int step4 = KM >= 4 ? k : 4;
@@ -308,8 +314,12 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
   const int x0 = xb * kW;
   const int y0 = a.row0 + res + seg * a.walk * a.k;
   if (res >= a.k || y0 >= a.row0 + a.rows) return;  // uniform over the CTA
-  // Only CTAs at the left / right grid edge can hold a partly-outside quad.
-  const bool fix = (KM < 4 || (a.N & 3)) && (xb == 0 || xb == a.xblocks - 1);
+  // CTAs whose quads can be partly outside the grid (a quad that straddles N, or k < 4 at
+  // the left edge) take the per-element path; for k >= 4 and N % 4 == 0 a neighbour quad
+  // is either wholly inside or wholly outside the grid, and the latter is exact as a
+  // centre-quad substitution.
+  const int step4 = KM >= 4 ? a.k : 4;
+  const bool fix = (KM < 4 || (a.N & 3)) && (x0 < step4 + 4 || x0 + kW + step4 + 4 > a.N);
   if (fix) walk<KM, MAY_EMPTY, BANDED, true>(a, x0, y0, dyn_smem);
   else walk<KM, MAY_EMPTY, BANDED, false>(a, x0, y0, dyn_smem);
 }

@@ -54,7 +54,7 @@ def test_jfa_extras_bit_exact(vd, extras):
     assert np.array_equal(d.labels(), oracle.jfa(N, xy, extras))
 
 
-@pytest.mark.parametrize("N", [2, 3, 5, 8, 13, 64, 100, 257, 1024])
+@pytest.mark.parametrize("N", [2, 3, 5, 8, 13, 64, 100, 257, 1024, 1031, 2051])
 def test_single_pass_random_states_bit_exact(vd, N):
     # One pass from arbitrary label maps (seeds and EMPTY mixed, not only reachable
     # states), for every k regime: 1, 2, multiples of 4, >= 512 and non-powers of two
