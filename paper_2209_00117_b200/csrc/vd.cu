@@ -275,6 +275,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
   const uint32_t C = 2 * h->N - 1;
   a.vempty = (C << 16) | C;
   a.sh16 = 65536u;
+  a.one = 1u;
   vd_status st = timed_begin(h);
   if (st) return st;
   if (fast_ok(h->N, may_empty) && (k & (k - 1)) == 0) {

@@ -13,12 +13,15 @@
 namespace vdk {
 
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-constexpr int kThreads = 128;  // threads per CTA in the pass kernels (4 px each -> 512 columns)
-#ifndef VD_MIN_BLOCKS
-#define VD_MIN_BLOCKS 4        // CTAs per SM the register allocation must allow
+#ifndef VD_THREADS
+#define VD_THREADS 128
 #endif
-#ifndef VD_DY_ALU
-#define VD_DY_ALU 1            // 1: dy on the ALU pipe (LEA.HI), 0: on the FMA pipe (IMAD.HI)
+constexpr int kThreads = VD_THREADS;  // threads per CTA in the fast pass kernel (4 px each)
+#ifndef VD_MIN_BLOCKS
+#define VD_MIN_BLOCKS (512 / VD_THREADS)  // CTAs per SM the register allocation must allow
+#endif
+#ifndef VD_DY_FMA
+#define VD_DY_FMA 0            // how many of the nine dy per pixel are computed on the FMA pipe
 #endif
 
 // ------------------------------------------------------------------ arguments
@@ -41,6 +44,7 @@ struct PassArgs {
   int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
+  uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
 };
 
 __device__ __forceinline__ const uint32_t* row_ptr(const PassArgs& a, int r) {
@@ -107,7 +111,7 @@ constexpr int kW = 4 * kThreads;         // columns per CTA
 #define VD_MAX_WALK 16
 #endif
 #ifndef VD_SMEM_KB
-#define VD_SMEM_KB 48
+#define VD_SMEM_KB (48 * VD_THREADS / 128)
 #endif
 constexpr int kMaxWalk = VD_MAX_WALK;    // output rows per walk (upper bound)
 constexpr int kSmemBudget = VD_SMEM_KB * 1024;  // staged rows per CTA
@@ -184,7 +188,7 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
 }
 
 __device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const Row& Cn, int e,
-                                              uint32_t negy, uint32_t sh16) {
+                                              uint32_t negy, uint32_t sh16, uint32_t one) {
   uint32_t c[9], d[9];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
@@ -194,11 +198,12 @@ __device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const 
   }
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
-#if VD_DY_ALU
-    const int dy = (int)((c[i] >> 16) + negy);                 // (c >> 16) - y  (LEA.HI, ALU pipe)
-#else
-    const int dy = (int)mad_hi_u32(c[i], sh16, negy);         // (c >> 16) - y  (IMAD.HI, FMA pipe)
-#endif
+    // dy = (c >> 16) - y.  The first VD_DY_FMA of the nine run on the FMA pipe
+    // (IMAD.HI for c >> 16, IMAD for the subtraction), the rest on the ALU pipe (one
+    // LEA.HI), to balance the two integer pipes.
+    int dy;
+    if (i < VD_DY_FMA) dy = (int)(__umulhi(c[i], sh16) * one + negy);
+    else dy = (int)((c[i] >> 16) + negy);
     d[i] = (uint32_t)(dy * dy) + d[i];
   }
   const uint32_t m = __vimin3_u32(__vimin3_u32(d[0], d[1], d[2]), __vimin3_u32(d[3], d[4], d[5]),
@@ -288,7 +293,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     uint32_t o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      uint32_t v = best_of_9(P, C, Nx, e, negy, sh16);
+      uint32_t v = best_of_9(P, C, Nx, e, negy, sh16, a.one);
       if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
       o[e] = v;
     }

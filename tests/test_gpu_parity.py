@@ -244,3 +244,19 @@ def test_c4_bench_config_full_grid(vd):
         best = ((ly[d2 == m].astype(np.uint32) << 16) | lx[d2 == m].astype(np.uint32)).min()
         good += int(L[y, x] == best)
     assert good >= 396  # P:268 "nearly 100%"
+
+
+@pytest.mark.parametrize("N", [16384, 20000])
+def test_empty_never_wins_at_large_n(vd, N):
+    # R-21 / R-4: a single seed in the far corner; every JFA pass compares EMPTY (key +inf)
+    # against that seed at the largest distances the grid allows.  One-seed JFA is exact,
+    # so every pixel must end with the seed.  16384 is the largest N of the fast kernel's
+    # EMPTY variant (virtual far seed), 20000 runs the 64-bit kernel.
+    xy = np.array([N - 1, N - 1], dtype=np.uint16)
+    d = _jfa_gpu(vd, N, xy)
+    L = d.labels()
+    assert (L == oracle.pack(N - 1, N - 1)).all()
+    xy = np.array([0, 0], dtype=np.uint16)
+    d2 = _jfa_gpu(vd, N, xy)
+    assert d2.match_count(d2) == N * N
+    assert (d2.labels() == 0).all()
