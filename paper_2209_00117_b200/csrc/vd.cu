@@ -117,6 +117,7 @@ struct Shard {
 
 struct vd_ctx {
   int device = 0;
+  int num_sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   uint32_t N = 0;
@@ -250,6 +251,7 @@ cudaError_t set_smem_attrs() {
   VD_ATTR(2, true, true) VD_ATTR(2, true, false) VD_ATTR(2, false, true) VD_ATTR(2, false, false)
   VD_ATTR(4, true, true) VD_ATTR(4, true, false) VD_ATTR(4, false, true) VD_ATTR(4, false, false)
 #undef VD_ATTR
+
   done = e;
   return e;
 }
@@ -519,6 +521,10 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   if (cfg.device >= 0) h->device = cfg.device;
   else if (cudaGetDevice(&h->device) != cudaSuccess) { delete h; return VD_ERR_CUDA; }
   DeviceGuard guard(h->device);
+  if (cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) {
+    delete h;
+    return VD_ERR_CUDA;
+  }
 
   auto bail = [&](vd_status st) {
     free_all(h);
@@ -630,33 +636,36 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   if (!disp_xy) return VD_ERR_ARG;
   if (!h->has_diagram) return fail(h, VD_ERR_STATE, "vd_djfa_step needs a diagram: call vd_jfa first");
   DeviceGuard guard(h->device);
-  if (!h->fwd) CK(cudaMalloc(&h->fwd, (size_t)h->N * h->N * sizeof(uint32_t)));
+  if (!h->fwd) {  // forward map, kept all-EMPTY between steps
+    CK(cudaMalloc(&h->fwd, (size_t)h->N * h->N * sizeof(uint32_t)));
+    CK(cudaMemsetAsync(h->fwd, 0xFF, (size_t)h->N * h->N * sizeof(uint32_t), h->stream));
+  }
   std::vector<uint32_t> ks;
   schedule_djfa(h->N, h->s, d_max, h->extras, ks);
-  // 1. SimulateParticles
-  vd_status st = move_seeds(h, disp_xy);
+  vd_status st = upload_disp(h, disp_xy);
   if (st) return st;
-  // 2. forward map old -> new (R-9)
   const int gs = grid_for((int64_t)h->s, 256);
-  vdk::fwd_clear<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, (int64_t)h->s);
-  if ((st = after_launch(h, "fwd_clear"))) return st;
-  vdk::fwd_min<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, h->seeds_new, (int64_t)h->s);
-  if ((st = after_launch(h, "fwd_min"))) return st;
-  // 3. labels follow their seeds (reuse of VD_{t-1})
+  // 1. SimulateParticles + forward map old -> new (R-9); fwd is all EMPTY on entry
+  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, h->disp, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N);
+  if ((st = after_launch(h, "move_fwd"))) return st;
+  // 2. labels follow their seeds (reuse of VD_{t-1})
   for (auto& sh : h->shards) {
     const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
     vdk::remap<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd);
     if ((st = after_launch(h, "remap"))) return st;
   }
-  // 4. re-stamp the new seed pixels
-  std::swap(h->seeds, h->seeds_new);
-  if ((st = stamp_all(h, h->seeds))) return st;
-  // 5. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
-  //    seed), so no EMPTY exists.
-  for (uint32_t k : ks) {
-    st = run_pass(h, k, false);
-    if (st) return st;
+  // 3. re-stamp the new seed pixels; fwd back to all-EMPTY
+  for (size_t g = 0; g < h->shards.size(); ++g) {
+    Shard& sh = h->shards[g];
+    vdk::reset_stamp<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, h->seeds_new, sh.buf[h->cur], h->pitch,
+                                                (int)sh.row0, (int)sh.rows, (int64_t)h->s, g == 0 ? 1 : 0);
+    if ((st = after_launch(h, "reset_stamp"))) return st;
   }
+  std::swap(h->seeds, h->seeds_new);
+  // 4. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
+  //    seed), so no EMPTY exists.
+  for (uint32_t k : ks)
+    if ((st = run_pass(h, k, false))) return st;
   h->last_passes = (uint32_t)ks.size();
   return VD_OK;
 }

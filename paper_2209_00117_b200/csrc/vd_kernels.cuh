@@ -405,19 +405,39 @@ __global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __r
   }
 }
 
-// Forward map (R-9): fwd[old_i] <- min over seeds j at the same old pixel of new_j.
-// Step 1 clears the entries at old seed pixels, step 2 takes the atomic minimum.
-__global__ void fwd_clear(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s, int64_t s) {
+// SimulateParticles (Alg. 1) fused with the forward map (R-9):
+// new = clamp(old + disp) per axis (R-10; the reserved pixel at N = 65536, R-4), then
+// fwd[old] <- min(fwd[old], new): co-located seeds leave the smallest new label.  fwd is
+// all EMPTY between dJFA steps (reset_stamp restores it).
+__global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __restrict__ disp,
+                         uint32_t* __restrict__ new_s, uint32_t* __restrict__ fwd, int64_t s, int N) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t c = old_s[i];
-    fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)] = EMPTY;
+    const uint32_t c = old_s[i];
+    const short2 d = disp[i];
+    int x = (int)(c & 0xFFFFu) + d.x, y = (int)(c >> 16) + d.y;
+    x = min(max(x, 0), N - 1);
+    y = min(max(y, 0), N - 1);
+    if (N == 65536 && x == 65535 && y == 65535) x = 65534;
+    const uint32_t nw = ((uint32_t)y << 16) | (uint32_t)x;
+    new_s[i] = nw;
+    atomicMin(&fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)], nw);
   }
 }
-__global__ void fwd_min(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s,
-                        const uint32_t* __restrict__ new_s, int64_t s) {
+
+// After the remap: restore fwd to all-EMPTY (its entries at the old seed pixels) and
+// re-stamp the new seed pixels of this band (R-9: remap, then re-stamp).  Co-located seeds
+// write the same values, so the unordered writes are benign.
+__global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s,
+                            const uint32_t* __restrict__ new_s, uint32_t* __restrict__ g, int64_t pitch, int row0,
+                            int rows, int64_t s, int do_reset) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t c = old_s[i];
-    atomicMin(&fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)], new_s[i]);
+    if (do_reset) {
+      const uint32_t o = old_s[i];
+      fwd[(int64_t)(o >> 16) * N + (o & 0xFFFFu)] = EMPTY;
+    }
+    const uint32_t c = new_s[i];
+    const int y = (int)(c >> 16) - row0, x = (int)(c & 0xFFFFu);
+    if (y >= 0 && y < rows) g[(int64_t)y * pitch + x] = c;
   }
 }
 
