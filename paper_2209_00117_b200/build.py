@@ -21,7 +21,7 @@ def _nccl_include() -> str:
 def nvcc_cmd(out: str = LIB, extra: list[str] | None = None) -> list[str]:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     return [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-            "-cudart", "static", "-Xptxas", "-warn-spills",
+            "-cudart", "static",
             "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
             "-o", out, *SRC, "-ldl", *(extra or [])]
 

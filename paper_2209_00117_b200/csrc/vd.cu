@@ -273,7 +273,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
   a.top_row0 = (int)sh.row0 - (int)k;
   a.bot_row0 = (int)(sh.row0 + d * B);
   a.k = (int)k;
-  a.xblocks = (int)((h->N + 4 * vdk::kThreads - 1) / (4 * vdk::kThreads));
+  a.xblocks = (int)((h->N + vdk::kW - 1) / vdk::kW);  // 512-column chunks (fast pass)
   const uint32_t C = 2 * h->N - 1;
   a.vempty = (C << 16) | C;
   a.sh16 = 65536u;

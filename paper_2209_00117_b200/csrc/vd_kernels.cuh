@@ -13,15 +13,13 @@
 namespace vdk {
 
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-#ifndef VD_THREADS
-#define VD_THREADS 128
+#ifndef VD_VEC
+#define VD_VEC 4               // labels per thread in the fast pass (2 or 4): one 64/128-bit access
 #endif
-constexpr int kThreads = VD_THREADS;  // threads per CTA in the fast pass kernel (4 px each)
+constexpr int kVec = VD_VEC;
+constexpr int kThreads = 512 / kVec;  // threads per CTA of the fast pass: a CTA covers 512 columns
 #ifndef VD_MIN_BLOCKS
-#define VD_MIN_BLOCKS (512 / VD_THREADS)  // CTAs per SM the register allocation must allow
-#endif
-#ifndef VD_DY_FMA
-#define VD_DY_FMA 0            // how many of the nine dy per pixel are computed on the FMA pipe
+#define VD_MIN_BLOCKS 4        // CTAs per SM the register allocation must allow (VEC=4: 128 regs, a few spills)
 #endif
 
 // ------------------------------------------------------------------ arguments
@@ -94,9 +92,16 @@ __device__ __forceinline__ uint32_t get(const uint4& v, int e) {
 //    (C << 16) | C, C = 2N - 1 <= 32767: a point farther from every pixel than any real
 //    seed (min d2 = 2 N^2 > 2 (N-1)^2), still a label < 2^31 above every real label, and
 //    mapped back to EMPTY on store.  Requires N <= 16384.
+// One input row as seen by one thread, for its kVec output columns x..x+kVec-1: for each
+// output column e, the labels of input columns x+e-k (L), x+e (C), x+e+k (R), and per
+// label cy and Q = cy^2 + (cx - (x+e))^2.  For an output pixel (x+e, y) every candidate
+// then has d2 - y^2 = Q - 2 y cy: ONE integer multiply-add per candidate, and since y^2
+// is common to the nine candidates of a pixel the minimum and every difference m - d2
+// (hence the tie-break) are unchanged.
 struct Row {
-  uint32_t c[12];   // labels: [0..3] column x+e-k, [4..7] x+e, [8..11] x+e+k (e = 0..3)
-  uint32_t dx2[12]; // (cx - (x+e))^2 for the matching output column x+e
+  uint32_t c[3 * kVec];  // labels: [0, kVec) L, [kVec, 2 kVec) C, [2 kVec, 3 kVec) R
+  int32_t cy[3 * kVec];  // c >> 16
+  int32_t q[3 * kVec];   // cy^2 + (cx - (x+e))^2
 };
 
 __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t c) {
@@ -106,12 +111,12 @@ __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t 
 }
 
 // ---- shared-memory row staging with cp.async.bulk (TMA bulk copies) -----------------
-constexpr int kW = 4 * kThreads;         // columns per CTA
+constexpr int kW = kVec * kThreads;      // columns per CTA (512)
 #ifndef VD_MAX_WALK
 #define VD_MAX_WALK 16
 #endif
 #ifndef VD_SMEM_KB
-#define VD_SMEM_KB (48 * VD_THREADS / 128)
+#define VD_SMEM_KB 48
 #endif
 constexpr int kMaxWalk = VD_MAX_WALK;    // output rows per walk (upper bound)
 constexpr int kSmemBudget = VD_SMEM_KB * 1024;  // staged rows per CTA
@@ -156,61 +161,69 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Build one Row (labels + dx^2) for output columns x..x+3 from a staged input row.
-// li / ci / ri: element offsets of the left / centre / right quads in the stage.
+template <int V>
+struct VecT;
+template <>
+struct VecT<2> { using T = uint2; };
+template <>
+struct VecT<4> { using T = uint4; };
+
+__device__ __forceinline__ void unpack(const uint2& v, uint32_t* w) { w[0] = v.x; w[1] = v.y; }
+__device__ __forceinline__ void unpack(const uint4& v, uint32_t* w) { w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
+
+// Build one Row from a staged input row.  li / ci / ri: element offsets of the left /
+// centre / right vectors in the stage.  KM = min(k, kVec): KM == kVec means the neighbour
+// vectors at x -+ k are aligned; KM < kVec takes the neighbours from the adjacent vectors.
 template <int KM, bool MAY_EMPTY, bool FIX>
 __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, int li, int ci, int ri, int x, int k,
-                                              int N, uint32_t vempty, uint32_t sh16, const int (&xs16)[4], Row& R) {
-  const uint4 Lv = *reinterpret_cast<const uint4*>(st + li);
-  const uint4 C = *reinterpret_cast<const uint4*>(st + ci);
-  const uint4 Rv = *reinterpret_cast<const uint4*>(st + ri);
-  const uint32_t w[12] = {Lv.x, Lv.y, Lv.z, Lv.w, C.x, C.y, C.z, C.w, Rv.x, Rv.y, Rv.z, Rv.w};
+                                              int N, uint32_t vempty, uint32_t sh16, const int (&xs16)[kVec], Row& R) {
+  using V = typename VecT<kVec>::T;
+  uint32_t w[3 * kVec];
+  unpack(*reinterpret_cast<const V*>(st + li), w);
+  unpack(*reinterpret_cast<const V*>(st + ci), w + kVec);
+  unpack(*reinterpret_cast<const V*>(st + ri), w + 2 * kVec);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    if constexpr (KM >= 4) { R.c[e] = w[e]; R.c[8 + e] = w[8 + e]; }
-    else { R.c[e] = w[4 + e - KM]; R.c[8 + e] = w[4 + e + KM]; }
-    R.c[4 + e] = w[4 + e];
+  for (int e = 0; e < kVec; ++e) {
+    if constexpr (KM >= kVec) { R.c[e] = w[e]; R.c[2 * kVec + e] = w[2 * kVec + e]; }
+    else { R.c[e] = w[kVec + e - KM]; R.c[2 * kVec + e] = w[kVec + e + KM]; }
+    R.c[kVec + e] = w[kVec + e];
   }
   if constexpr (FIX) {  // an out-of-grid column -> the pixel's own column (a duplicate)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (x + e - k < 0) R.c[e] = w[4 + e];
-      if (x + e + k >= N) R.c[8 + e] = w[4 + e];
+    for (int e = 0; e < kVec; ++e) {
+      if (x + e - k < 0) R.c[e] = w[kVec + e];
+      if (x + e + k >= N) R.c[2 * kVec + e] = w[kVec + e];
     }
   }
 #pragma unroll
-  for (int i = 0; i < 12; ++i) {
+  for (int i = 0; i < 3 * kVec; ++i) {
     uint32_t c = R.c[i];
     if (MAY_EMPTY) { c = __vminu2(c, vempty); R.c[i] = c; }  // EMPTY -> virtual far seed
-    const int D = (int)(c * sh16) + xs16[i & 3];              // (cx - (x+e)) << 16
-    R.dx2[i] = (uint32_t)__mulhi(D, D);                       // (cx - (x+e))^2
+    const int D = (int)(c * sh16) + xs16[i % kVec];           // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
+    const int cy = (int)(c >> 16);
+    R.cy[i] = cy;
+    R.q[i] = cy * cy + __mulhi(D, D);                          // cy^2 + dx^2
   }
 }
 
-__device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const Row& Cn, int e,
-                                              uint32_t negy, uint32_t sh16, uint32_t one) {
-  uint32_t c[9], d[9];
+// Output label of pixel (x+e, y): candidates = column e of the three rows.  With
+// d'_i = d2_i - y^2 = Q_i - 2 y cy_i (int32, may be negative): m = min d'_i (signed), then
+// out = min_i max(c_i, m - d'_i) in uint32 -- for d'_i = m the term is c_i, for d'_i > m the
+// difference m - d'_i = m2 - d2_i wraps to >= 2^31, above every label in use (< 2^31).
+__device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const Row& Cn, int e, int n2y) {
+  uint32_t c[9];
+  int d[9];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    c[j] = A.c[4 * j + e];  d[j] = A.dx2[4 * j + e];
-    c[3 + j] = B.c[4 * j + e];  d[3 + j] = B.dx2[4 * j + e];
-    c[6 + j] = Cn.c[4 * j + e]; d[6 + j] = Cn.dx2[4 * j + e];
+    c[j] = A.c[kVec * j + e];     d[j] = A.q[kVec * j + e] + A.cy[kVec * j + e] * n2y;
+    c[3 + j] = B.c[kVec * j + e]; d[3 + j] = B.q[kVec * j + e] + B.cy[kVec * j + e] * n2y;
+    c[6 + j] = Cn.c[kVec * j + e]; d[6 + j] = Cn.q[kVec * j + e] + Cn.cy[kVec * j + e] * n2y;
   }
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    // dy = (c >> 16) - y.  The first VD_DY_FMA of the nine run on the FMA pipe
-    // (IMAD.HI for c >> 16, IMAD for the subtraction), the rest on the ALU pipe (one
-    // LEA.HI), to balance the two integer pipes.
-    int dy;
-    if (i < VD_DY_FMA) dy = (int)(__umulhi(c[i], sh16) * one + negy);
-    else dy = (int)((c[i] >> 16) + negy);
-    d[i] = (uint32_t)(dy * dy) + d[i];
-  }
-  const uint32_t m = __vimin3_u32(__vimin3_u32(d[0], d[1], d[2]), __vimin3_u32(d[3], d[4], d[5]),
-                                  __vimin3_u32(d[6], d[7], d[8]));
+  const int m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), __vimin3_s32(d[3], d[4], d[5]),
+                             __vimin3_s32(d[6], d[7], d[8]));
   uint32_t w[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) w[i] = __viaddmax_u32(m, 0u - d[i], c[i]);  // max(m - d_i, c_i)
+  for (int i = 0; i < 9; ++i) w[i] = __viaddmax_u32((uint32_t)m, 0u - (uint32_t)d[i], c[i]);  // max(m - d_i, c_i)
   return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]),
                       __vimin3_u32(w[6], w[7], w[8]));
 }
@@ -228,7 +241,7 @@ template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX>
 __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t* smem) {
   const int k = a.k, N = a.N;
   const int tid = (int)threadIdx.x;
-  const int x = x0 + 4 * tid;
+  const int x = x0 + kVec * tid;
   const int yend = a.row0 + a.rows;
   const int nout = min(a.walk, (yend - y0 + k - 1) / k);  // output rows of this walk
   const int nlist = nout + 2;                              // staged input rows
@@ -265,13 +278,15 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     }
   }
 
-  // quad offsets in a stage (out-of-grid neighbour quads -> the centre quad)
-  const int step4 = KM >= 4 ? k : 4;
-  const int ci = spans3 ? kW + 4 * tid : K4 + 4 * tid;
-  const int li = (x - step4 >= 0) ? (spans3 ? 4 * tid : ci - step4) : ci;
-  const int ri = (x + step4 < N) ? (spans3 ? 2 * kW + 4 * tid : ci + step4) : ci;
-  const uint32_t sh16 = a.sh16;  // 65536, from memory so ptxas keeps the multiplies on the FMA pipe
-  const int xs16[4] = {-(x << 16), -((x + 1) << 16), -((x + 2) << 16), -((x + 3) << 16)};
+  // vector offsets in a stage (out-of-grid neighbour vectors -> the centre vector)
+  const int nstep = KM >= kVec ? k : kVec;  // distance to the neighbour vectors
+  const int ci = spans3 ? kW + kVec * tid : K4 + kVec * tid;
+  const int li = (x - nstep >= 0) ? (spans3 ? kVec * tid : ci - nstep) : ci;
+  const int ri = (x + nstep < N) ? (spans3 ? 2 * kW + kVec * tid : ci + nstep) : ci;
+  const uint32_t sh16 = a.sh16;  // 65536, from memory so ptxas keeps the multiply on the FMA pipe
+  int xs16[kVec];
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) xs16[e] = -((x + e) << 16);
   const bool active = x < N;
 
   auto consume = [&](int i, Row& R) {
@@ -287,17 +302,21 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   const int64_t kp = (int64_t)k * a.pitch;
   int j = 0;
   // Output row j: P = row j (y-k), C = row j+1 (y), Nx <- row j+2 (y+k).
+  using V = typename VecT<kVec>::T;
   auto step = [&](const Row& P, const Row& C, Row& Nx) -> bool {
     consume(j + 2, Nx);
-    const uint32_t negy = 0u - (uint32_t)y;
-    uint32_t o[4];
+    const int n2y = -2 * y;
+    uint32_t o[kVec];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t v = best_of_9(P, C, Nx, e, negy, sh16, a.one);
+    for (int e = 0; e < kVec; ++e) {
+      uint32_t v = best_of_9(P, C, Nx, e, n2y);
       if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
       o[e] = v;
     }
-    if (active) *reinterpret_cast<uint4*>(po) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (active) {
+      if constexpr (kVec == 4) *reinterpret_cast<uint4*>(po) = make_uint4(o[0], o[1], o[2], o[3]);
+      else *reinterpret_cast<uint2*>(po) = make_uint2(o[0], o[1]);
+    }
     po += kp;
     y += k;
     return ++j < nout;
@@ -319,12 +338,12 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
   const int x0 = xb * kW;
   const int y0 = a.row0 + res + seg * a.walk * a.k;
   if (res >= a.k || y0 >= a.row0 + a.rows) return;  // uniform over the CTA
-  // CTAs whose quads can be partly outside the grid (a quad that straddles N, or k < 4 at
-  // the left edge) take the per-element path; for k >= 4 and N % 4 == 0 a neighbour quad
-  // is either wholly inside or wholly outside the grid, and the latter is exact as a
-  // centre-quad substitution.
-  const int step4 = KM >= 4 ? a.k : 4;
-  const bool fix = (KM < 4 || (a.N & 3)) && (x0 < step4 + 4 || x0 + kW + step4 + 4 > a.N);
+  // CTAs whose vectors can be partly outside the grid (a vector that straddles N, or
+  // k < kVec at the left edge) take the per-element path; for k >= kVec and N % kVec == 0
+  // a neighbour vector is either wholly inside or wholly outside the grid, and the latter
+  // is exact as a centre-vector substitution.
+  const int nstep = KM >= kVec ? a.k : kVec;
+  const bool fix = (KM < kVec || (a.N & (kVec - 1))) && (x0 < nstep + kVec || x0 + kW + nstep + kVec > a.N);
   if (fix) walk<KM, MAY_EMPTY, BANDED, true>(a, x0, y0, dyn_smem);
   else walk<KM, MAY_EMPTY, BANDED, false>(a, x0, y0, dyn_smem);
 }
