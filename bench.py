@@ -205,14 +205,17 @@ def run_gpu(args):
         return float(t.item())
 
     N, s, d, cdesc = CONFIGS[args.config]
-    nccl_id = None
-    if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(vd.vd_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
-    cfg = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
+
+    def handle_cfg():
+        # every libvd handle gets its own NCCL communicator, hence its own unique id
+        nccl_id = None
+        if world > 1:
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(vd.vd_nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nccl_id = bytes(idt.cpu().numpy().tobytes())
+        return dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
 
     xy0 = synth.uniform_seeds(N, s, rng_seed=RNG)
     W, K = args.warmup, args.steps
@@ -226,8 +229,8 @@ def run_gpu(args):
         return torch.cuda.Event(enable_timing=True)
 
     # ---------------- dJFA: bootstrap (untimed), warmup, timed region
-    dj = vd.VoronoiDiagram(N, xy0, **cfg)
-    jf = vd.VoronoiDiagram(N, xy0, **cfg)
+    dj = vd.VoronoiDiagram(N, xy0, **handle_cfg())
+    jf = vd.VoronoiDiagram(N, xy0, **handle_cfg())
     dj.jfa()
     for f in range(W):
         dj.djfa_step(disp_dev[f], d)

@@ -23,6 +23,7 @@ import threading
 import numpy as np
 
 EMPTY = 0xFFFFFFFF
+METRICS = {"euclid": 0, "manhattan": 1}  # P:172-173 (dJFAe / dJFAm)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "vd_oracle.c")
@@ -71,6 +72,10 @@ def _load():
             "or_match_count": (u64, [u64, p, p]),
             "or_label_hash": (u64, [u64, p]),
             "or_num_threads": (i32, []),
+            "or_pass_v": (None, [u32, u32, i32, i32, p, p]),
+            "or_exact_brute_m": (None, [u32, u64, p, i32, p]),
+            "or_jfa_v": (i32, [u32, u64, p, u32, i32, i32, p]),
+            "or_djfa_step_v": (i32, [u32, u64, p, p, u32, u32, i32, i32, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -114,11 +119,12 @@ def djfa_schedule(N: int, s: int, d_max: int, extras: int = 0) -> list[int]:
     return [int(v) for v in ks[:n]]
 
 
-def exact_brute(N: int, xy) -> np.ndarray:
-    """Eq. 1 by brute force over all seeds; (N, N) uint32 labels."""
+def exact_brute(N: int, xy, metric: str = "euclid") -> np.ndarray:
+    """Eq. 1 by brute force over all seeds; (N, N) uint32 labels.
+    metric: "euclid" (default, P:173) or "manhattan" (dJFAm, P:172-173)."""
     xy = _seeds(xy)
     out = np.empty((N, N), dtype=np.uint32)
-    _load().or_exact_brute(N, xy.size // 2, _ptr(xy), _ptr(out))
+    _load().or_exact_brute_m(N, xy.size // 2, _ptr(xy), METRICS[metric], _ptr(out))
     return out
 
 
@@ -143,21 +149,23 @@ def init(N: int, xy) -> np.ndarray:
     return G
 
 
-def jump_pass(G: np.ndarray, k: int) -> np.ndarray:
-    """One gather pass with step k over Table 1; returns a new array."""
+def jump_pass(G: np.ndarray, k: int, metric: str = "euclid", vn: bool = False) -> np.ndarray:
+    """One gather pass with step k over Table 1; returns a new array.
+    vn: Von Neumann neighbourhood (the 4 axis offsets)."""
     G = np.ascontiguousarray(G, dtype=np.uint32)
     N = G.shape[0]
     assert G.shape == (N, N)
     out = np.empty_like(G)
-    _load().or_pass(N, k, _ptr(G), _ptr(out))
+    _load().or_pass_v(N, k, METRICS[metric], int(bool(vn)), _ptr(G), _ptr(out))
     return out
 
 
-def jfa(N: int, xy, extras: int = 0) -> np.ndarray:
-    """Full JFA: init + passes of jfa_schedule(N, extras)."""
+def jfa(N: int, xy, extras: int = 0, metric: str = "euclid", vn_waves: int = 0) -> np.ndarray:
+    """Full JFA: init + passes of jfa_schedule(N, extras); the first vn_waves passes use
+    the Von Neumann neighbourhood ("Von Neumann alone ... even for JFA")."""
     xy = _seeds(xy)
     G = np.empty((N, N), dtype=np.uint32)
-    n = _load().or_jfa(N, xy.size // 2, _ptr(xy), extras, _ptr(G))
+    n = _load().or_jfa_v(N, xy.size // 2, _ptr(xy), extras, METRICS[metric], vn_waves, _ptr(G))
     if n < 0:
         raise ValueError("or_jfa failed")
     return G
@@ -173,15 +181,17 @@ def move(N: int, xy_old, disp) -> np.ndarray:
     return out
 
 
-def djfa_step(N: int, xy_old, disp, d_max: int, G: np.ndarray, extras: int = 0):
-    """One dJFA time step (Alg. 1; R-9).  Returns (G_new, xy_new, passes)."""
+def djfa_step(N: int, xy_old, disp, d_max: int, G: np.ndarray, extras: int = 0, metric: str = "euclid",
+              vn_waves: int = 0):
+    """One dJFA time step (Alg. 1; R-9).  Returns (G_new, xy_new, passes).
+    metric "manhattan" = dJFAm; vn_waves = Von Neumann waves first."""
     xy_old = _seeds(xy_old)
     disp = np.ascontiguousarray(disp, dtype=np.int16).reshape(-1)
     assert disp.size == xy_old.size
     G = np.array(G, dtype=np.uint32, copy=True, order="C")
     xy_new = np.empty_like(xy_old)
-    n = _load().or_djfa_step(N, xy_old.size // 2, _ptr(xy_old), _ptr(disp), d_max, extras,
-                             _ptr(G), _ptr(xy_new))
+    n = _load().or_djfa_step_v(N, xy_old.size // 2, _ptr(xy_old), _ptr(disp), d_max, extras, METRICS[metric],
+                               vn_waves, _ptr(G), _ptr(xy_new))
     if n == -3:
         raise ValueError("previous diagram is incomplete or holds non-seed labels")
     if n < 0:

@@ -39,17 +39,32 @@ static uint64_t dist2(uint32_t x, uint32_t y, uint32_t c) {
     return (uint64_t)(dx * dx) + (uint64_t)(dy * dy);
 }
 
+/* Manhattan distance |dx| + |dy| (dJFAm: "not having square roots neither
+ * squared values"). */
+static uint64_t dist1(uint32_t x, uint32_t y, uint32_t c) {
+    int64_t dx = (int64_t)x - (int64_t)label_x(c);
+    int64_t dy = (int64_t)y - (int64_t)label_y(c);
+    return (uint64_t)(dx < 0 ? -dx : dx) + (uint64_t)(dy < 0 ? -dy : dy);
+}
+
+/* The distance a metric compares: OR_EUCLID -> squared Euclidean (same order as the
+ * Euclidean distance), OR_MANHATTAN -> Manhattan. */
+static uint64_t dist_m(uint32_t x, uint32_t y, uint32_t c, int metric) {
+    return metric == OR_MANHATTAN ? dist1(x, y, c) : dist2(x, y, c);
+}
+
 /* Does candidate label c beat the current best label b at pixel (x, y)?
- * key(p, c) < key(p, b) lexicographically on (d2, label); EMPTY is +infinity (R-3, R-4).
+ * key(p, c) < key(p, b) lexicographically on (distance, label); EMPTY is +infinity (R-3, R-4).
  * "the distance function is used as a criterion to check which flood carries
  * the closest seed". */
-static int better(uint32_t x, uint32_t y, uint32_t c, uint32_t b) {
+static int better_m(uint32_t x, uint32_t y, uint32_t c, uint32_t b, int metric) {
     if (c == OR_EMPTY) return 0;
     if (b == OR_EMPTY) return 1;
-    uint64_t dc = dist2(x, y, c), db = dist2(x, y, b);
+    uint64_t dc = dist_m(x, y, c, metric), db = dist_m(x, y, b, metric);
     if (dc != db) return dc < db;
     return c < b;
 }
+static int better(uint32_t x, uint32_t y, uint32_t c, uint32_t b) { return better_m(x, y, c, b, OR_EUCLID); }
 
 /* ---------------------------------------------------------------- schedules */
 
@@ -116,18 +131,21 @@ int or_djfa_schedule(uint32_t N, uint64_t s, uint32_t d_max, uint32_t extras, ui
 
 /* Eq. 1: R_k = {x : d(x, P_k) <= d(x, P_j) for all j}.  Brute force: every
  * pixel scans every seed and keeps the minimum key (R-3 picks one region on ties). */
-void or_exact_brute(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t* out) {
+void or_exact_brute_m(uint32_t N, uint64_t s, const uint16_t* xy, int metric, uint32_t* out) {
 #pragma omp parallel for schedule(static)
     for (int64_t y = 0; y < (int64_t)N; y++) {
         for (uint32_t x = 0; x < N; x++) {
             uint32_t best = OR_EMPTY;
             for (uint64_t i = 0; i < s; i++) {
                 uint32_t c = or_pack(xy[2 * i], xy[2 * i + 1]);
-                if (better(x, (uint32_t)y, c, best)) best = c;
+                if (better_m(x, (uint32_t)y, c, best, metric)) best = c;
             }
             out[(uint64_t)y * N + x] = best;
         }
     }
+}
+void or_exact_brute(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t* out) {
+    or_exact_brute_m(N, s, xy, OR_EUCLID, out);
 }
 
 /* Same result as or_exact_brute (tests check equality), found faster: seeds are put in
@@ -200,44 +218,56 @@ static const int MOORE[8][2] = {{+1, 0}, {+1, +1}, {0, +1}, {-1, +1},
  *   out[p] = argmin_key over {in[p]} U {in[p + o*k] : o in Table 1, p + o*k inside the grid}
  * Out-of-grid neighbours are skipped (R-11).  This is Alg. 1's per-pixel body
  * with the roles of p and q exchanged: pixel p takes the closest seed among
- * the seeds its neighbours carry (S:177 proves the equivalence; tests check it). */
-void or_pass(uint32_t N, uint32_t k, const uint32_t* in, uint32_t* out) {
+ * the seeds its neighbours carry (S:177 proves the equivalence; tests check it).
+ * vn != 0: Von Neumann neighbourhood, the 4 axis offsets of Table 1 (neighbours 1, 3, 5,
+ * 7; "explore half the neighbors compared to Moore").  metric: OR_EUCLID or
+ * OR_MANHATTAN. */
+void or_pass_v(uint32_t N, uint32_t k, int metric, int vn, const uint32_t* in, uint32_t* out) {
 #pragma omp parallel for schedule(static)
     for (int64_t y = 0; y < (int64_t)N; y++) {
         for (int64_t x = 0; x < (int64_t)N; x++) {
             uint32_t best = in[(uint64_t)y * N + (uint64_t)x];
             for (int j = 0; j < 8; j++) {
+                if (vn && (j & 1)) continue; /* Table 1 neighbours 2, 4, 6, 8 are diagonal */
                 int64_t qx = x + (int64_t)MOORE[j][0] * k;
                 int64_t qy = y + (int64_t)MOORE[j][1] * k;
                 if (qx < 0 || qy < 0 || qx >= (int64_t)N || qy >= (int64_t)N) continue;
                 uint32_t c = in[(uint64_t)qy * N + (uint64_t)qx];
-                if (better((uint32_t)x, (uint32_t)y, c, best)) best = c;
+                if (better_m((uint32_t)x, (uint32_t)y, c, best, metric)) best = c;
             }
             out[(uint64_t)y * N + (uint64_t)x] = best;
         }
     }
 }
+void or_pass(uint32_t N, uint32_t k, const uint32_t* in, uint32_t* out) { or_pass_v(N, k, OR_EUCLID, 0, in, out); }
 
-/* Run the passes of ks[0..n) on G (in place, using `tmp` as the other buffer). */
-static void run_passes(uint32_t N, const uint32_t* ks, int n, uint32_t* G, uint32_t* tmp) {
+/* Run the passes of ks[0..n) on G (in place, using `tmp` as the other buffer); the first
+ * vn_waves passes use the Von Neumann neighbourhood, the rest Moore (P:170, P:188,
+ * P:204 "Von Neumann for the first two waves, Moore for the rest"). */
+static void run_passes_v(uint32_t N, const uint32_t* ks, int n, int metric, int vn_waves, uint32_t* G,
+                         uint32_t* tmp) {
     uint64_t np = (uint64_t)N * N;
     for (int i = 0; i < n; i++) {
-        or_pass(N, ks[i], G, tmp);
+        or_pass_v(N, ks[i], metric, i < vn_waves, G, tmp);
         memcpy(G, tmp, np * sizeof(uint32_t));
     }
 }
 
-/* Full JFA: init, then passes k_1, ..., 1 (+ extras).  Returns #passes. */
-int or_jfa(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t extras, uint32_t* G) {
+/* Full JFA: init, then passes k_1, ..., 1 (+ extras).  Returns #passes.
+ * metric / vn_waves as in run_passes_v (Euclidean Moore JFA: OR_EUCLID, 0). */
+int or_jfa_v(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t extras, int metric, int vn_waves, uint32_t* G) {
     uint32_t ks[64];
     int n = or_jfa_schedule(N, extras, ks, 64);
     if (n < 0 || s == 0) return -1;
     uint32_t* tmp = (uint32_t*)malloc((uint64_t)N * N * sizeof(uint32_t));
     if (!tmp) return -2;
     or_init(N, s, xy, G);
-    run_passes(N, ks, n, G, tmp);
+    run_passes_v(N, ks, n, metric, vn_waves, G, tmp);
     free(tmp);
     return n;
+}
+int or_jfa(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t extras, uint32_t* G) {
+    return or_jfa_v(N, s, xy, extras, OR_EUCLID, 0, G);
 }
 
 /* ---------------------------------------------------------------- dJFA */
@@ -265,11 +295,12 @@ void or_move(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp
  *   2. fwd[P(old_i)] = min over {j : old_j = old_i} of P(new_j)      (labels follow seeds)
  *   3. G[p] <- fwd[G[p]] for every pixel (G must be complete: every label an old seed)
  *   4. G[P(new_i)] <- P(new_i)                                         (re-stamp)
- *   5. passes delta_1, ..., 1 (+ extras) from Eq. 4, as or_pass.
+ *   5. passes delta_1, ..., 1 (+ extras) from Eq. 4, as or_pass_v (metric; the first
+ *      vn_waves of them Von Neumann).
  * Returns the number of passes, or -3 if G held a label that is not an old seed position
  * ("rejects incomplete prev"). */
-int or_djfa_step(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp,
-                 uint32_t d_max, uint32_t extras, uint32_t* G, uint16_t* xy_new) {
+int or_djfa_step_v(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp, uint32_t d_max,
+                   uint32_t extras, int metric, int vn_waves, uint32_t* G, uint16_t* xy_new) {
     uint32_t ks[64];
     int n = or_djfa_schedule(N, s, d_max, extras, ks, 64);
     if (n < 0) return -1;
@@ -302,9 +333,14 @@ int or_djfa_step(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* 
     for (uint64_t i = 0; i < s; i++)
         G[(uint64_t)xy_new[2 * i + 1] * N + xy_new[2 * i]] = or_pack(xy_new[2 * i], xy_new[2 * i + 1]);
 
-    run_passes(N, ks, n, G, tmp);
+    run_passes_v(N, ks, n, metric, vn_waves, G, tmp);
     free(fwd); free(tmp);
     return n;
+}
+
+int or_djfa_step(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp,
+                 uint32_t d_max, uint32_t extras, uint32_t* G, uint16_t* xy_new) {
+    return or_djfa_step_v(N, s, xy_old, disp, d_max, extras, OR_EUCLID, 0, G, xy_new);
 }
 
 /* ---------------------------------------------------------------- metrics */

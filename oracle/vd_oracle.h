@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #define OR_EMPTY 0xFFFFFFFFu
+#define OR_EUCLID 0
+#define OR_MANHATTAN 1
 
 uint32_t or_pack(uint32_t x, uint32_t y);
 int or_jfa_schedule(uint32_t N, uint32_t extras, uint32_t* ks, int cap);
@@ -14,6 +16,11 @@ void or_exact_brute(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t* out);
 int or_exact_bucketed(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t bs, uint32_t* out);
 void or_init(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t* G);
 void or_pass(uint32_t N, uint32_t k, const uint32_t* in, uint32_t* out);
+void or_pass_v(uint32_t N, uint32_t k, int metric, int vn, const uint32_t* in, uint32_t* out);
+void or_exact_brute_m(uint32_t N, uint64_t s, const uint16_t* xy, int metric, uint32_t* out);
+int or_jfa_v(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t extras, int metric, int vn_waves, uint32_t* G);
+int or_djfa_step_v(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp, uint32_t d_max,
+                   uint32_t extras, int metric, int vn_waves, uint32_t* G, uint16_t* xy_new);
 int or_jfa(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t extras, uint32_t* G);
 void or_move(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp, uint16_t* xy_new);
 int or_djfa_step(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* disp,
