@@ -64,6 +64,9 @@ enum {
 };
 
 #define VD_EMPTY 0xFFFFFFFFu
+#define VD_METRIC_EUCLIDEAN 0u
+#define VD_METRIC_MANHATTAN 1u
+#define VD_PASS_VON_NEUMANN 1u
 
 typedef struct {
     int32_t device;         /* CUDA ordinal; -1 = the calling thread's current device      */
@@ -74,10 +77,18 @@ typedef struct {
     uint32_t extra_passes;  /* trailing k = 1 passes after JFA / dJFA schedules (P:114,
                                P:150 "An extra step may be included"); default 0 (R-6)     */
     uint32_t virtual_shards;/* > 1: emulate that many row bands in this handle (world = 1) */
-    uint32_t reserved[6];   /* must be zero                                                */
+    uint32_t metric;        /* VD_METRIC_EUCLIDEAN (default, dJFAe) or VD_METRIC_MANHATTAN
+                               (dJFAm); used by every pass of the handle         */
+    uint32_t vn_waves;      /* the first vn_waves passes of each vd_djfa_step use the Von
+                               Neumann neighbourhood (the 4 axis offsets of Table 1), the
+                               rest Moore ("Von Neumann for the first two
+                               waves"); default 0 = Moore only                              */
+    uint32_t jfa_vn_waves;  /* same for vd_jfa (Fig. 5 / P:163-168: Von Neumann-only JFA)   */
+    uint32_t reserved[3];   /* must be zero                                                */
 } vd_config;
 
-/* Fill *cfg with defaults: device -1, stream NULL, rank 0, world 1, no extras. */
+/* Fill *cfg with defaults: device -1, stream NULL, rank 0, world 1, no extras,
+ * Euclidean metric, Moore neighbourhood. */
 void vd_config_init(vd_config* cfg);
 
 /* Write a fresh 128-byte ncclUniqueId to out128 (rank 0 calls it, then broadcasts the
@@ -123,9 +134,11 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max);
 vd_status vd_set_labels(vd_handle h, const uint32_t* labels);
 
 /* One jump pass with step k >= 1 on the current diagram (the body of every JFA / dJFA
- * wave, in gather form R-12), including the halo exchange when sharded.
- * Powers of two use the fast kernel; any other k the generic one (same results). */
-vd_status vd_pass(vd_handle h, uint32_t k);
+ * wave, in gather form R-12), including the halo exchange when sharded, with
+ * the handle's metric.  flags: VD_PASS_VON_NEUMANN = only the 4 axis neighbours
+ * (P:154-160), else the Moore 8 of Table 1.  Powers of two use the fast kernel; any
+ * other k the generic one (same results). */
+vd_status vd_pass(vd_handle h, uint32_t k, uint32_t flags);
 
 /* Eq. 5: 100 * matching pixels / total pixels between the diagrams of h and
  * ref (same N and sharding; ref may be h).  *matches (optional) gets the integer count.

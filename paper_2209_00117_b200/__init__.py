@@ -52,7 +52,10 @@ class vd_config(ctypes.Structure):
         ("nccl_id", ctypes.c_void_p),
         ("extra_passes", ctypes.c_uint32),
         ("virtual_shards", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32 * 6),
+        ("metric", ctypes.c_uint32),
+        ("vn_waves", ctypes.c_uint32),
+        ("jfa_vn_waves", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32 * 3),
     ]
 
 
@@ -96,7 +99,7 @@ _SIGS = {
     "vd_halo_plan": (ctypes.c_int32, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                                       ctypes.POINTER(vd_halo_plan_t)]),
     "vd_set_labels": (ctypes.c_int32, [H, P]),
-    "vd_pass": (ctypes.c_int32, [H, ctypes.c_uint32]),
+    "vd_pass": (ctypes.c_int32, [H, ctypes.c_uint32, ctypes.c_uint32]),
     "vd_destroy": (None, [H]),
     "vd_status_str": (ctypes.c_char_p, [ctypes.c_int32]),
     "vd_last_error": (ctypes.c_char_p, [H]),
@@ -158,8 +161,13 @@ def vd_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+METRICS = {"euclid": 0, "manhattan": 1}  # VD_METRIC_* (dJFAe / dJFAm)
+VD_PASS_VON_NEUMANN = 1
+
+
 def vd_create(N: int, seeds_xy, *, device: int = -1, stream: int | None = None, rank: int = 0, world: int = 1,
-              nccl_id: bytes | None = None, extra_passes: int = 0, virtual_shards: int = 0):
+              nccl_id: bytes | None = None, extra_passes: int = 0, virtual_shards: int = 0, metric: str = "euclid",
+              vn_waves: int = 0, jfa_vn_waves: int = 0):
     lib = load_library()
     s = (seeds_xy.numel() if hasattr(seeds_xy, "numel") else np.asarray(seeds_xy).size) // 2
     ptr, keep = _addr(seeds_xy, np.uint16, 2 * s)
@@ -174,6 +182,9 @@ def vd_create(N: int, seeds_xy, *, device: int = -1, stream: int | None = None, 
         cfg.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     cfg.extra_passes = extra_passes
     cfg.virtual_shards = virtual_shards
+    cfg.metric = METRICS[metric]
+    cfg.vn_waves = vn_waves
+    cfg.jfa_vn_waves = jfa_vn_waves
     h = H()
     _check(lib.vd_create(ctypes.byref(h), N, s, ptr, ctypes.byref(cfg)), "vd_create")
     del keep, idbuf
@@ -206,8 +217,8 @@ def vd_set_labels(h, labels: np.ndarray) -> None:
     _check(load_library().vd_set_labels(h, ctypes.c_void_p(arr.ctypes.data)), "vd_set_labels", h)
 
 
-def vd_pass(h, k: int) -> None:
-    _check(load_library().vd_pass(h, k), "vd_pass", h)
+def vd_pass(h, k: int, von_neumann: bool = False) -> None:
+    _check(load_library().vd_pass(h, k, VD_PASS_VON_NEUMANN if von_neumann else 0), "vd_pass", h)
 
 
 def vd_similarity(h, ref) -> tuple[float, int]:
@@ -357,8 +368,8 @@ class VoronoiDiagram:
     def set_labels(self, labels):
         vd_set_labels(self.h, labels)
 
-    def jump_pass(self, k: int):
-        vd_pass(self.h, k)
+    def jump_pass(self, k: int, von_neumann: bool = False):
+        vd_pass(self.h, k, von_neumann)
 
     def labels(self) -> np.ndarray:
         return vd_get_labels(self.h, self.N)

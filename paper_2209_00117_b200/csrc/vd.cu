@@ -126,6 +126,9 @@ struct vd_ctx {
   int rank = 0, world = 1;
   uint32_t vshards = 1;
   uint32_t extras = 0;
+  int metric = 0;           // 0 Euclidean (dJFAe), 1 Manhattan (dJFAm)
+  uint32_t vn_waves = 0;    // Von Neumann waves at the start of each dJFA step
+  uint32_t jfa_vn_waves = 0;// ... and of each full JFA (Fig. 5)
   uint32_t hcap = 0;  // halo rows allocated per side
   std::vector<Shard> shards;
   int cur = 0;        // which ping-pong buffer holds the diagram
@@ -239,26 +242,34 @@ vd_status timed_end(vd_ctx* h, uint64_t px) {
 }
 
 // Which kernel variant can take this pass exactly (see vd_kernels.cuh).
-// Opt every fast-pass instantiation into the largest staging size (vdk::pass_smem).
-cudaError_t set_smem_attrs() {
-  static cudaError_t done = cudaErrorNotReady;
-  if (done != cudaErrorNotReady) return done;
-  cudaError_t e = cudaSuccess;
-  const int bytes = vdk::kSmemBudget;  // pass_smem(k) <= kSmemBudget for every k
-#define VD_ATTR(KM, ME, BD) \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  VD_ATTR(1, true, true) VD_ATTR(1, true, false) VD_ATTR(1, false, true) VD_ATTR(1, false, false)
-  VD_ATTR(2, true, true) VD_ATTR(2, true, false) VD_ATTR(2, false, true) VD_ATTR(2, false, false)
-  VD_ATTR(4, true, true) VD_ATTR(4, true, false) VD_ATTR(4, false, true) VD_ATTR(4, false, false)
-#undef VD_ATTR
-
-  done = e;
-  return e;
+// Launch one fast-pass instantiation; each opts into the largest staging size once.
+template <int KM, bool ME, bool BD, int MT, bool VN>
+cudaError_t launch_fast(const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
+  static cudaError_t attr = cudaErrorNotReady;
+  if (attr == cudaErrorNotReady)
+    attr = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                vdk::kSmemBudget);
+  if (attr != cudaSuccess) return attr;
+  vdk::jump_pass_fast<KM, ME, BD, MT, VN><<<grid, blk, sm, st>>>(a);
+  return cudaSuccess;
+}
+template <int KM, bool ME, bool BD>
+cudaError_t launch_fast_mv(int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
+  if (metric == 0) return vn ? launch_fast<KM, ME, BD, 0, true>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 0, false>(a, g, b, sm, st);
+  return vn ? launch_fast<KM, ME, BD, 1, true>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 1, false>(a, g, b, sm, st);
+}
+template <int KM>
+cudaError_t launch_fast_k(bool me, bool bd, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm,
+                          cudaStream_t st) {
+  if (me) return bd ? launch_fast_mv<KM, true, true>(metric, vn, a, g, b, sm, st)
+                    : launch_fast_mv<KM, true, false>(metric, vn, a, g, b, sm, st);
+  return bd ? launch_fast_mv<KM, false, true>(metric, vn, a, g, b, sm, st)
+            : launch_fast_mv<KM, false, false>(metric, vn, a, g, b, sm, st);
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
 
-vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
+vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn) {
   vdk::PassArgs a;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
@@ -278,6 +289,8 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
   a.vempty = (C << 16) | C;
   a.sh16 = 65536u;
   a.one = 1u;
+  a.metric = h->metric;
+  a.vn = vn ? 1 : 0;
   vd_status st = timed_begin(h);
   if (st) return st;
   if (fast_ok(h->N, may_empty) && (k & (k - 1)) == 0) {
@@ -288,22 +301,12 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
     const bool banded = sh.top != nullptr;
-    CK(set_smem_attrs());
     const size_t sm = vdk::pass_smem((int)k);
-#define VD_LAUNCH(KM)                                                                        \
-  do {                                                                                       \
-    if (may_empty) {                                                                         \
-      if (banded) vdk::jump_pass_fast<KM, true, true><<<grid, blk, sm, h->stream>>>(a);     \
-      else vdk::jump_pass_fast<KM, true, false><<<grid, blk, sm, h->stream>>>(a);           \
-    } else {                                                                                 \
-      if (banded) vdk::jump_pass_fast<KM, false, true><<<grid, blk, sm, h->stream>>>(a);    \
-      else vdk::jump_pass_fast<KM, false, false><<<grid, blk, sm, h->stream>>>(a);          \
-    }                                                                                        \
-  } while (0)
-    if (k == 1) VD_LAUNCH(1);
-    else if (k == 2) VD_LAUNCH(2);
-    else VD_LAUNCH(4);
-#undef VD_LAUNCH
+    cudaError_t e;
+    if (k == 1) e = launch_fast_k<1>(may_empty, banded, h->metric, vn, a, grid, blk, sm, h->stream);
+    else if (k == 2) e = launch_fast_k<2>(may_empty, banded, h->metric, vn, a, grid, blk, sm, h->stream);
+    else e = launch_fast_k<4>(may_empty, banded, h->metric, vn, a, grid, blk, sm, h->stream);
+    CK(e);
   } else {
     a.segs = 1;
     a.walk = 1;
@@ -316,7 +319,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty) {
 }
 
 // Halo exchange for step k (vd_halo_plan), then one pass on every local shard.
-vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty) {
+vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
   const size_t row_bytes = (size_t)h->pitch * sizeof(uint32_t);
   if (h->world > 1) {
     vd_halo_plan_t p;
@@ -347,7 +350,7 @@ vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty) {
     }
   }
   for (auto& sh : h->shards) {
-    vd_status st = launch_pass(h, sh, k, may_empty);
+    vd_status st = launch_pass(h, sh, k, may_empty, vn);
     if (st) return st;
   }
   h->cur ^= 1;
@@ -491,8 +494,9 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   if (cfg.world > 1 && vsh > 1) return VD_ERR_ARG;
   if (G > 1 && (!pow2 || N % G != 0 || (G & (G - 1)) != 0)) return VD_ERR_ARG;
   if (cfg.world > 1 && !cfg.nccl_id) return VD_ERR_ARG;
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 3; ++i)
     if (cfg.reserved[i]) return VD_ERR_ARG;
+  if (cfg.metric > 1) return VD_ERR_ARG;
 
   // Validate and pack the seeds on the host (R-1, R-4).
   std::vector<uint16_t> hxy;
@@ -518,6 +522,9 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   h->world = cfg.world;
   h->vshards = cfg.world > 1 ? 1 : vsh;
   h->extras = cfg.extra_passes;
+  h->metric = (int)cfg.metric;
+  h->vn_waves = cfg.vn_waves;
+  h->jfa_vn_waves = cfg.jfa_vn_waves;
   if (cfg.device >= 0) h->device = cfg.device;
   else if (cudaGetDevice(&h->device) != cudaSuccess) { delete h; return VD_ERR_CUDA; }
   DeviceGuard guard(h->device);
@@ -611,8 +618,8 @@ vd_status vd_jfa(vd_handle h) {
   if (st) return st;
   // EMPTY can survive until the diagram is complete; the fast kernel's EMPTY variant
   // is used for every JFA pass (it is exact either way).
-  for (uint32_t k : ks) {
-    st = run_pass(h, k, true);
+  for (size_t i = 0; i < ks.size(); ++i) {
+    st = run_pass(h, ks[i], true, i < h->jfa_vn_waves);
     if (st) return st;
   }
   h->last_passes = (uint32_t)ks.size();
@@ -664,8 +671,8 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   std::swap(h->seeds, h->seeds_new);
   // 4. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
   //    seed), so no EMPTY exists.
-  for (uint32_t k : ks)
-    if ((st = run_pass(h, k, false))) return st;
+  for (size_t i = 0; i < ks.size(); ++i)
+    if ((st = run_pass(h, ks[i], false, i < h->vn_waves))) return st;
   h->last_passes = (uint32_t)ks.size();
   return VD_OK;
 }
@@ -694,7 +701,7 @@ vd_status vd_set_labels(vd_handle h, const uint32_t* labels) {
   return VD_OK;
 }
 
-vd_status vd_pass(vd_handle h, uint32_t k) {
+vd_status vd_pass(vd_handle h, uint32_t k, uint32_t flags) {
   CHECK_HANDLE(h);
   if (k == 0 || k >= 65536) return VD_ERR_ARG;
   DeviceGuard guard(h->device);
@@ -704,7 +711,7 @@ vd_status vd_pass(vd_handle h, uint32_t k) {
     if (k > B && k % B != 0) return fail(h, VD_ERR_ARG, "sharded pass needs k < band rows or a multiple of them");
     if (k > h->hcap && k < B) return fail(h, VD_ERR_ARG, "halo capacity exceeded");
   }
-  return run_pass(h, k, true);
+  return run_pass(h, k, true, (flags & VD_PASS_VON_NEUMANN) != 0);
 }
 
 vd_status vd_similarity(vd_handle h, vd_handle ref, double* pct, uint64_t* matches) {

@@ -43,6 +43,8 @@ struct PassArgs {
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
+  int32_t metric;   // 0 Euclidean, 1 Manhattan (jump_pass_wide; the fast kernel templates it)
+  int32_t vn;       // Von Neumann neighbourhood (jump_pass_wide)
 };
 
 __device__ __forceinline__ const uint32_t* row_ptr(const PassArgs& a, int r) {
@@ -174,7 +176,8 @@ __device__ __forceinline__ void unpack(const uint4& v, uint32_t* w) { w[0] = v.x
 // Build one Row from a staged input row.  li / ci / ri: element offsets of the left /
 // centre / right vectors in the stage.  KM = min(k, kVec): KM == kVec means the neighbour
 // vectors at x -+ k are aligned; KM < kVec takes the neighbours from the adjacent vectors.
-template <int KM, bool MAY_EMPTY, bool FIX>
+// METRIC 0: Euclidean (q = cy^2 + dx^2); METRIC 1: Manhattan, dJFAm (q = |dx|).
+template <int KM, bool MAY_EMPTY, bool FIX, int METRIC>
 __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, int li, int ci, int ri, int x, int k,
                                               int N, uint32_t vempty, uint32_t sh16, const int (&xs16)[kVec], Row& R) {
   using V = typename VecT<kVec>::T;
@@ -199,33 +202,55 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
   for (int i = 0; i < 3 * kVec; ++i) {
     uint32_t c = R.c[i];
     if (MAY_EMPTY) { c = __vminu2(c, vempty); R.c[i] = c; }  // EMPTY -> virtual far seed
-    const int D = (int)(c * sh16) + xs16[i % kVec];           // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
     const int cy = (int)(c >> 16);
     R.cy[i] = cy;
-    R.q[i] = cy * cy + __mulhi(D, D);                          // cy^2 + dx^2
+    if constexpr (METRIC == 0) {
+      const int D = (int)(c * sh16) + xs16[i % kVec];         // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
+      R.q[i] = cy * cy + __mulhi(D, D);                        // cy^2 + dx^2
+    } else {
+      R.q[i] = (int)__sad((int)(c & 0xFFFFu), x + (i % kVec), 0u);  // |cx - (x+e)|
+    }
   }
 }
 
-// Output label of pixel (x+e, y): candidates = column e of the three rows.  With
-// d'_i = d2_i - y^2 = Q_i - 2 y cy_i (int32, may be negative): m = min d'_i (signed), then
-// out = min_i max(c_i, m - d'_i) in uint32 -- for d'_i = m the term is c_i, for d'_i > m the
-// difference m - d'_i = m2 - d2_i wraps to >= 2^31, above every label in use (< 2^31).
-__device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const Row& Cn, int e, int n2y) {
+// Output label of pixel (x+e, y): candidates = column e of the three rows (Moore), or
+// only the centre column of the rows above / below plus the centre row (Von Neumann,
+// P:154-160).  Euclidean: d'_i = d2_i - y^2 = Q_i - 2 y cy_i (int32, may be negative; y^2
+// is common to all candidates of the pixel).  Manhattan: d_i = |cy_i - y| + |dx_i|.
+// m = min d_i (signed), then out = min_i max(c_i, m - d_i) in uint32 -- for d_i = m the
+// term is c_i, for d_i > m the difference wraps to >= 2^31, above every label in use
+// (< 2^31).
+template <int METRIC, bool VN>
+__device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Row& Cn, int e, int y) {
+  constexpr int n = VN ? 5 : 9;
   uint32_t c[9];
   int d[9];
+  auto dist = [&](const Row& R, int i) -> int {
+    if constexpr (METRIC == 0) return R.q[i] + R.cy[i] * (-2 * y);
+    else return (int)__sad(R.cy[i], y, (unsigned)R.q[i]);
+  };
+  if constexpr (!VN) {
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    c[j] = A.c[kVec * j + e];     d[j] = A.q[kVec * j + e] + A.cy[kVec * j + e] * n2y;
-    c[3 + j] = B.c[kVec * j + e]; d[3 + j] = B.q[kVec * j + e] + B.cy[kVec * j + e] * n2y;
-    c[6 + j] = Cn.c[kVec * j + e]; d[6 + j] = Cn.q[kVec * j + e] + Cn.cy[kVec * j + e] * n2y;
+    for (int j = 0; j < 3; ++j) {
+      c[j] = A.c[kVec * j + e];     d[j] = dist(A, kVec * j + e);
+      c[3 + j] = B.c[kVec * j + e]; d[3 + j] = dist(B, kVec * j + e);
+      c[6 + j] = Cn.c[kVec * j + e]; d[6 + j] = dist(Cn, kVec * j + e);
+    }
+  } else {
+    c[0] = A.c[kVec + e];  d[0] = dist(A, kVec + e);
+    c[1] = Cn.c[kVec + e]; d[1] = dist(Cn, kVec + e);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) { c[2 + j] = B.c[kVec * j + e]; d[2 + j] = dist(B, kVec * j + e); }
   }
-  const int m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), __vimin3_s32(d[3], d[4], d[5]),
-                             __vimin3_s32(d[6], d[7], d[8]));
+  int m;
+  if constexpr (VN) m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), d[3], d[4]);
+  else m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), __vimin3_s32(d[3], d[4], d[5]), __vimin3_s32(d[6], d[7], d[8]));
   uint32_t w[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) w[i] = __viaddmax_u32((uint32_t)m, 0u - (uint32_t)d[i], c[i]);  // max(m - d_i, c_i)
-  return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]),
-                      __vimin3_u32(w[6], w[7], w[8]));
+  for (int i = 0; i < n; ++i) w[i] = __viaddmax_u32((uint32_t)m, 0u - (uint32_t)d[i], c[i]);  // max(m - d_i, c_i)
+  if constexpr (VN) return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), w[3], w[4]);
+  else return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]),
+                           __vimin3_u32(w[6], w[7], w[8]));
 }
 
 // One CTA = 512 columns x one walk (up to kMaxWalk output rows of one residue class
@@ -237,7 +262,7 @@ __device__ __forceinline__ uint32_t best_of_9(const Row& A, const Row& B, const 
 // the centre row (the producer stages that row again), columns outside the grid by the
 // pixel's own column: duplicates never change a minimum.
 // BANDED: rows beyond the band come from the halo buffers (row_ptr).
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX>
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, int METRIC, bool VN>
 __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t* smem) {
   const int k = a.k, N = a.N;
   const int tid = (int)threadIdx.x;
@@ -291,7 +316,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
 
   auto consume = [&](int i, Row& R) {
     mbar_wait(&bars[i], 0u);
-    row_from_smem<KM, MAY_EMPTY, FIX>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16, R);
+    row_from_smem<KM, MAY_EMPTY, FIX, METRIC>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16, R);
   };
 
   Row r0, r1, r2;
@@ -305,11 +330,10 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   using V = typename VecT<kVec>::T;
   auto step = [&](const Row& P, const Row& C, Row& Nx) -> bool {
     consume(j + 2, Nx);
-    const int n2y = -2 * y;
     uint32_t o[kVec];
 #pragma unroll
     for (int e = 0; e < kVec; ++e) {
-      uint32_t v = best_of_9(P, C, Nx, e, n2y);
+      uint32_t v = best_of<METRIC, VN>(P, C, Nx, e, y);
       if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
       o[e] = v;
     }
@@ -329,7 +353,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   }
 }
 
-template <int KM, bool MAY_EMPTY, bool BANDED>
+template <int KM, bool MAY_EMPTY, bool BANDED, int METRIC = 0, bool VN = false>
 __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
@@ -344,8 +368,8 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
   // is exact as a centre-vector substitution.
   const int nstep = KM >= kVec ? a.k : kVec;
   const bool fix = (KM < kVec || (a.N & (kVec - 1))) && (x0 < nstep + kVec || x0 + kW + nstep + kVec > a.N);
-  if (fix) walk<KM, MAY_EMPTY, BANDED, true>(a, x0, y0, dyn_smem);
-  else walk<KM, MAY_EMPTY, BANDED, false>(a, x0, y0, dyn_smem);
+  if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN>(a, x0, y0, dyn_smem);
+  else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN>(a, x0, y0, dyn_smem);
 }
 
 // ------------------------------------------------------------------ wide jump pass
@@ -353,10 +377,11 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
 // Same pass for grids the fast kernel cannot take exactly (N > 32768, or EMPTY present
 // with N > 23170): uint64 squared distances, explicit EMPTY, lexicographic (d2, label).
 // One thread per 4 adjacent pixels of one row, nine 128-bit loads.
-__device__ __forceinline__ void consider_wide(uint32_t c, int x, int y, uint64_t& bd, uint32_t& bc) {
+__device__ __forceinline__ void consider_wide(uint32_t c, int x, int y, int metric, uint64_t& bd, uint32_t& bc) {
   if (c == EMPTY) return;
   int64_t dx = (int64_t)(c & 0xFFFFu) - x, dy = (int64_t)(c >> 16) - y;
-  uint64_t d = (uint64_t)(dx * dx) + (uint64_t)(dy * dy);
+  uint64_t d = metric == 0 ? (uint64_t)(dx * dx) + (uint64_t)(dy * dy)
+                           : (uint64_t)(dx < 0 ? -dx : dx) + (uint64_t)(dy < 0 ? -dy : dy);
   if (d < bd || (d == bd && c < bc)) { bd = d; bc = c; }
 }
 
@@ -377,11 +402,12 @@ __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
     const uint32_t* p = row_ptr(a, r);
 #pragma unroll
     for (int ox = -1; ox <= 1; ++ox) {
+      if (a.vn && ox != 0 && oy != 0) continue;  // Von Neumann: no diagonals
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         int q = x + e + ox * k;
         if (x + e >= N || q < 0 || q >= N) continue;
-        consider_wide(p[q], x + e, y, bd[e], best[e]);
+        consider_wide(p[q], x + e, y, a.metric, bd[e], best[e]);
       }
     }
   }

@@ -260,3 +260,45 @@ def test_empty_never_wins_at_large_n(vd, N):
     d2 = _jfa_gpu(vd, N, xy)
     assert d2.match_count(d2) == N * N
     assert (d2.labels() == 0).all()
+
+
+# ---------------------------------------------------------------- NEXT-2 variants
+# dJFAm (Manhattan) and Von Neumann waves, bit-exact
+# against the oracle's variant functions (pinned in tests/test_oracle_variants.py).
+
+@pytest.mark.parametrize("N", [5, 64, 257, 1024, 1031])
+@pytest.mark.parametrize("metric,vn", [("manhattan", False), ("euclid", True), ("manhattan", True)])
+def test_single_pass_variants_bit_exact(vd, N, metric, vn):
+    rng = np.random.default_rng(N + 7)
+    s = min(N * N, 40)
+    xy = synth.uniform_seeds(N, s, rng_seed=N)
+    labels = np.array([oracle.pack(int(xy[2 * i]), int(xy[2 * i + 1])) for i in range(s)] + [EMPTY], dtype=np.uint32)
+    d = vd.VoronoiDiagram(N, xy, metric=metric)
+    G = labels[rng.integers(0, len(labels), size=(N, N))]
+    for k in sorted({1, 2, 3, 4, 8, 64, 512} | {max(1, N // 2)}):
+        d.set_labels(G)
+        d.jump_pass(k, von_neumann=vn)
+        assert np.array_equal(d.labels(), oracle.jump_pass(G, k, metric=metric, vn=vn)), k
+
+
+@pytest.mark.parametrize("N,s", [(64, 16), (300, 100), (1024, 1024)])
+def test_jfa_variants_bit_exact(vd, N, s):
+    xy = synth.uniform_seeds(N, s, rng_seed=N * 3)
+    m = _jfa_gpu(vd, N, xy, metric="manhattan")
+    assert np.array_equal(m.labels(), oracle.jfa(N, xy, metric="manhattan"))
+    v = _jfa_gpu(vd, N, xy, jfa_vn_waves=99)  # Von Neumann-only JFA (Fig. 5): may stay incomplete
+    assert np.array_equal(v.labels(), oracle.jfa(N, xy, vn_waves=99))
+
+
+@pytest.mark.parametrize("metric,vn_waves", [("manhattan", 0), ("euclid", 2), ("manhattan", 2)])
+@pytest.mark.parametrize("N,s,dmax,G", [(64, 16, 1, 0), (1024, 1024, 2, 0), (512, 2048, 3, 4)])
+def test_djfa_variants_bit_exact(vd, metric, vn_waves, N, s, dmax, G):
+    xy = synth.uniform_seeds(N, s, rng_seed=N + s)
+    d = _jfa_gpu(vd, N, xy, metric=metric, vn_waves=vn_waves, virtual_shards=G)
+    ref = oracle.jfa(N, xy, metric=metric)
+    assert np.array_equal(d.labels(), ref)
+    for f in range(3):
+        disp = synth.displacements(s, dmax, f, rng_seed=N)
+        d.djfa_step(disp, dmax)
+        ref, xy, _ = oracle.djfa_step(N, xy, disp, dmax, ref, metric=metric, vn_waves=vn_waves)
+        assert np.array_equal(d.labels(), ref), f
