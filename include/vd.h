@@ -110,6 +110,12 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
  * Table 1, inside the grid} of the key (d2(p, c), c) (R-2, R-3, R-11). */
 vd_status vd_jfa(vd_handle h);
 
+/* Standard Flooding (Fig. 2a): the JFA initialisation, then k = 1 Moore passes
+ * (with the handle's metric) until no pixel is EMPTY -- the grid is "fully flooded"
+ * (reading R-22).  *passes (optional) gets the number of passes.  Synchronises once per
+ * pass (the stopping test reads an EMPTY count back). */
+vd_status vd_stf(vd_handle h, uint32_t* passes);
+
 /* SimulateParticles (Alg. 1) only: new = clamp(old + disp) per axis (R-10; at
  * N = 65536 a seed landing on (65535,65535) goes to (65534,65535), R-4).  disp_xy: s
  * int16 pairs, host or device.  Leaves the diagram stale (use before vd_jfa for the JFA

@@ -76,6 +76,7 @@ def _load():
             "or_exact_brute_m": (None, [u32, u64, p, i32, p]),
             "or_jfa_v": (i32, [u32, u64, p, u32, i32, i32, p]),
             "or_djfa_step_v": (i32, [u32, u64, p, p, u32, u32, i32, i32, p, p]),
+            "or_stf": (i32, [u32, u64, p, i32, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -169,6 +170,17 @@ def jfa(N: int, xy, extras: int = 0, metric: str = "euclid", vn_waves: int = 0) 
     if n < 0:
         raise ValueError("or_jfa failed")
     return G
+
+
+def stf(N: int, xy, metric: str = "euclid"):
+    """Standard Flooding: k = 1 Moore passes until no pixel is EMPTY (R-22).
+    Returns (G, passes)."""
+    xy = _seeds(xy)
+    G = np.empty((N, N), dtype=np.uint32)
+    n = _load().or_stf(N, xy.size // 2, _ptr(xy), METRICS[metric], _ptr(G))
+    if n < 0:
+        raise ValueError("or_stf failed")
+    return G, n
 
 
 def move(N: int, xy_old, disp) -> np.ndarray:

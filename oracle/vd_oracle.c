@@ -270,6 +270,29 @@ int or_jfa(uint32_t N, uint64_t s, const uint16_t* xy, uint32_t extras, uint32_t
     return or_jfa_v(N, s, xy, extras, OR_EUCLID, 0, G);
 }
 
+/* Standard Flooding (Fig. 2a): from the seed pixels, flood the neighbours at
+ * Chebyshev distance 1 (Moore, k = 1) in parallel, pass after pass, "until the grid is
+ * fully flooded" -- i.e. stop after the first pass that leaves no EMPTY pixel (reading
+ * R-22).  Returns the number of passes (0 if the seeds already cover the grid). */
+int or_stf(uint32_t N, uint64_t s, const uint16_t* xy, int metric, uint32_t* G) {
+    if (s == 0) return -1;
+    uint64_t np = (uint64_t)N * N;
+    uint32_t* tmp = (uint32_t*)malloc(np * sizeof(uint32_t));
+    if (!tmp) return -2;
+    or_init(N, s, xy, G);
+    int passes = 0;
+    while (1) {
+        uint64_t empty = 0;
+        for (uint64_t p = 0; p < np; p++) empty += (G[p] == OR_EMPTY);
+        if (empty == 0) break;
+        or_pass_v(N, 1, metric, 0, G, tmp);
+        memcpy(G, tmp, np * sizeof(uint32_t));
+        passes++;
+    }
+    free(tmp);
+    return passes;
+}
+
 /* ---------------------------------------------------------------- dJFA */
 
 /* SimulateParticles (Alg. 1): new = old + disp, clamped to the grid per axis

@@ -27,6 +27,7 @@ int or_djfa_step(uint32_t N, uint64_t s, const uint16_t* xy_old, const int16_t* 
                  uint32_t d_max, uint32_t extras, uint32_t* G, uint16_t* xy_new);
 uint64_t or_match_count(uint64_t np, const uint32_t* a, const uint32_t* b);
 uint64_t or_label_hash(uint64_t np, const uint32_t* g);
+int or_stf(uint32_t N, uint64_t s, const uint16_t* xy, int metric, uint32_t* G);
 int or_num_threads(void);
 
 #endif

@@ -21,7 +21,7 @@ import numpy as np
 __all__ = [
     "VDError", "load_library", "library_path", "VoronoiDiagram", "EMPTY",
     "vd_config", "vd_halo_plan_t", "vd_create", "vd_destroy", "vd_jfa", "vd_move_seeds",
-    "vd_djfa_step", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
+    "vd_djfa_step", "vd_stf", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
     "vd_get_seeds", "vd_band", "vd_last_passes", "vd_synchronize", "vd_set_pass_timing",
     "vd_pass_timing", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
     "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "EXPORTED_SYMBOLS",
@@ -78,6 +78,7 @@ _SIGS = {
     "vd_nccl_unique_id": (ctypes.c_int32, [P]),
     "vd_create": (ctypes.c_int32, [ctypes.POINTER(H), ctypes.c_uint32, ctypes.c_uint64, P, ctypes.POINTER(vd_config)]),
     "vd_jfa": (ctypes.c_int32, [H]),
+    "vd_stf": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32)]),
     "vd_move_seeds": (ctypes.c_int32, [H, P]),
     "vd_djfa_step": (ctypes.c_int32, [H, P, ctypes.c_uint32]),
     "vd_similarity": (ctypes.c_int32, [H, H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
@@ -198,6 +199,12 @@ def vd_destroy(h) -> None:
 
 def vd_jfa(h) -> None:
     _check(load_library().vd_jfa(h), "vd_jfa", h)
+
+
+def vd_stf(h) -> int:
+    n = ctypes.c_uint32()
+    _check(load_library().vd_stf(h, ctypes.byref(n)), "vd_stf", h)
+    return n.value
 
 
 def vd_move_seeds(h, disp_xy, s: int) -> None:
@@ -346,6 +353,9 @@ class VoronoiDiagram:
 
     def jfa(self):
         vd_jfa(self.h)
+
+    def stf(self) -> int:
+        return vd_stf(self.h)
 
     def move_seeds(self, disp_xy):
         vd_move_seeds(self.h, disp_xy, self.s)

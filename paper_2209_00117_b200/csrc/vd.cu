@@ -627,6 +627,38 @@ vd_status vd_jfa(vd_handle h) {
   return VD_OK;
 }
 
+vd_status vd_stf(vd_handle h, uint32_t* passes) {
+  CHECK_HANDLE(h);
+  DeviceGuard guard(h->device);
+  for (auto& sh : h->shards) {  // init as JFA: all EMPTY, seed pixels hold themselves
+    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
+    vdk::fill_empty<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4);
+    vd_status st = after_launch(h, "fill_empty");
+    if (st) return st;
+  }
+  vd_status st = stamp_all(h, h->seeds);
+  if (st) return st;
+  uint32_t n = 0;
+  while (true) {  // "until the grid is fully flooded": stop once no EMPTY is left
+    CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+    for (auto& sh : h->shards) {
+      const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
+      vdk::count_value<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+                                                                  VD_EMPTY, h->counter);
+      if ((st = after_launch(h, "count_value"))) return st;
+    }
+    uint64_t empty = 0;
+    if ((st = reduce_to_host(h, &empty))) return st;
+    if (empty == 0) break;
+    if ((st = run_pass(h, 1, true))) return st;
+    ++n;
+  }
+  h->last_passes = n;
+  h->has_diagram = true;
+  if (passes) *passes = n;
+  return VD_OK;
+}
+
 vd_status vd_move_seeds(vd_handle h, const int16_t* disp_xy) {
   CHECK_HANDLE(h);
   if (!disp_xy) return VD_ERR_ARG;

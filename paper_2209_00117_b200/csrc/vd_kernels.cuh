@@ -541,6 +541,23 @@ __global__ void match_count(const uint32_t* __restrict__ a, const uint32_t* __re
   if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
 }
 
+// Number of pixels of a band holding `value` (StF's "fully flooded" test with EMPTY).
+__global__ void count_value(const uint32_t* __restrict__ g, int64_t pitch, int rows, int N, uint32_t value,
+                            unsigned long long* __restrict__ out) {
+  const int xq = (N + 3) / 4;
+  const int64_t total = (int64_t)rows * xq;
+  uint64_t cnt = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / xq;
+    int x = (int)(i - r * xq) * 4;
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(g + r * pitch + x));
+    int nv = min(4, N - x);
+    cnt += (u.x == value) + (nv > 1 && u.y == value) + (nv > 2 && u.z == value) + (nv > 3 && u.w == value);
+  }
+  uint64_t t = block_sum_u64(cnt);
+  if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
+}
+
 __device__ __forceinline__ uint64_t smix(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -302,3 +302,35 @@ def test_djfa_variants_bit_exact(vd, metric, vn_waves, N, s, dmax, G):
         d.djfa_step(disp, dmax)
         ref, xy, _ = oracle.djfa_step(N, xy, disp, dmax, ref, metric=metric, vn_waves=vn_waves)
         assert np.array_equal(d.labels(), ref), f
+
+
+# ---------------------------------------------------------------- NEXT-4
+
+@pytest.mark.parametrize("N,s,metric", [(11, 1, "euclid"), (64, 16, "euclid"), (100, 7, "manhattan"), (257, 60, "euclid")])
+def test_stf_bit_exact(vd, N, s, metric):
+    # Standard Flooding: k = 1 passes until the grid is fully flooded (R-22)
+    xy = np.array([5, 5], dtype=np.uint16) if N == 11 else synth.uniform_seeds(N, s, rng_seed=N)
+    d = vd.VoronoiDiagram(N, xy, metric=metric)
+    n = d.stf()
+    G, n_ref = oracle.stf(N, xy, metric=metric)
+    assert n == n_ref and np.array_equal(d.labels(), G)
+    if N == 11:
+        assert n == 5  # P:76 "StF fulfills its purpose in 5 iterations"
+
+
+def test_paper_sample_run_1000x1000_50_seeds(vd):
+    # Fig. 6: "A 100 step simulation of 50 seeds on a grid of 1000x1000 pixels".
+    # Non-power-of-two grid; sparse seeds make delta_1 = k_1 ("behave very much like
+    # JFA").  All 100 frames bit-exact against the oracle.
+    N, s, dmax = 1000, 50, 4
+    xy = synth.uniform_seeds(N, s, rng_seed=6)
+    d = _jfa_gpu(vd, N, xy)
+    G = oracle.jfa(N, xy)
+    for f in range(100):
+        disp = synth.displacements(s, dmax, f, rng_seed=6)
+        d.djfa_step(disp, dmax)
+        G, xy, n = oracle.djfa_step(N, xy, disp, dmax, G)
+        assert n == len(oracle.jfa_schedule(N))
+        if f % 10 == 9:
+            assert d.label_hash() == oracle.label_hash(G), f
+    assert np.array_equal(d.labels(), G)

@@ -156,3 +156,31 @@ def test_zero_motion_manhattan_exact_is_identity():
     E = oracle.exact_brute(N, xy, metric="manhattan")
     G, _, _ = oracle.djfa_step(N, xy, np.zeros(2 * s, dtype=np.int16), 1, E, metric="manhattan", vn_waves=2)
     assert np.array_equal(G, E)
+
+
+# ---------------------------------------------------------------- Standard Flooding (NEXT-4)
+
+def test_stf_paper_example_five_iterations():
+    # P:76 / Fig. 2(a): "StF fulfills its purpose in 5 iterations" for one seed; a seed at
+    # the centre of an 11x11 grid is at Chebyshev distance 5 from the corners.
+    G, n = oracle.stf(11, np.array([5, 5], dtype=np.uint16))
+    assert n == 5 and (G == oracle.pack(5, 5)).all()
+
+
+@pytest.mark.parametrize("N,x,y", [(2, 0, 0), (7, 0, 0), (9, 2, 6), (16, 15, 3)])
+def test_stf_one_seed_passes_equal_chebyshev_radius(N, x, y):
+    # one seed floods the grid in max Chebyshev distance to a corner passes (closed form)
+    G, n = oracle.stf(N, np.array([x, y], dtype=np.uint16))
+    assert n == max(x, N - 1 - x, y, N - 1 - y)
+    assert (G == oracle.pack(x, y)).all()
+
+
+def test_stf_complete_and_close_to_exact():
+    # StF propagates claims one ring at a time; the result is complete and, like JFA,
+    # close to Eq. 1 (each pass is the same gather, R-12).
+    for r in range(6):
+        xy = synth.uniform_seeds(48, 10, rng_seed=40 + r)
+        G, n = oracle.stf(48, xy)
+        assert (G != EMPTY).all()
+        assert n <= 47
+        assert oracle.similarity(G, oracle.exact_brute(48, xy)) >= 97.0
