@@ -421,6 +421,41 @@ void free_all(vd_ctx* h) {
   h->stream = nullptr;
 }
 
+// JFA / StF initialisation: every pixel unclaimed, each seed pixel holds itself.
+// For N <= 16384 "unclaimed" is the virtual far seed V = (2N-1, 2N-1) instead of EMPTY:
+// V is farther from every pixel than any real seed and larger than every real label, so
+// in every pass it loses exactly as EMPTY (key +infinity) would, and the passes can run
+// the kernel variant without EMPTY handling.  Returns the value used.
+uint32_t unclaimed_label(const vd_ctx* h) {
+  const uint32_t C = 2 * h->N - 1;
+  return h->N <= 16384 ? ((C << 16) | C) : VD_EMPTY;
+}
+
+vd_status jfa_init(vd_ctx* h) {
+  const uint32_t u = unclaimed_label(h);
+  for (auto& sh : h->shards) {
+    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
+    vdk::fill_value<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u);
+    vd_status st = after_launch(h, "fill_value");
+    if (st) return st;
+  }
+  return stamp_all(h, h->seeds);
+}
+
+// V -> EMPTY for pixels no pass reached (Von Neumann-only waves can leave some, Fig. 5).
+vd_status jfa_finish(vd_ctx* h) {
+  const uint32_t u = unclaimed_label(h);
+  if (u == VD_EMPTY) return VD_OK;
+  for (auto& sh : h->shards) {
+    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
+    vdk::replace_value<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u,
+                                                                 VD_EMPTY);
+    vd_status st = after_launch(h, "replace_value");
+    if (st) return st;
+  }
+  return VD_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -608,38 +643,19 @@ vd_status vd_jfa(vd_handle h) {
   DeviceGuard guard(h->device);
   std::vector<uint32_t> ks;
   schedule_jfa(h->N, h->extras, ks);
-  for (auto& sh : h->shards) {  // JFA init: all EMPTY ...
-    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
-    vdk::fill_empty<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4);
-    vd_status st = after_launch(h, "fill_empty");
-    if (st) return st;
-  }
-  vd_status st = stamp_all(h, h->seeds);  // ... then each seed pixel holds its own label
+  vd_status st = jfa_init(h);
   if (st) return st;
-  // EMPTY can survive until the diagram is complete; the fast kernel's EMPTY variant
-  // is used for every JFA pass (it is exact either way).
+  const bool virt = unclaimed_label(h) != VD_EMPTY;
   for (size_t i = 0; i < ks.size(); ++i) {
-    st = run_pass(h, ks[i], true, i < h->jfa_vn_waves);
+    st = run_pass(h, ks[i], !virt, i < h->jfa_vn_waves);
     if (st) return st;
   }
+  // A Moore JFA reaches every pixel (k_1 = 2^(ceil(log2 N)-1) covers every offset), so no V
+  // survives; Von Neumann waves may leave some.
   h->last_passes = (uint32_t)ks.size();
-  h->has_diagram = true;
-  return VD_OK;
-}
-
-vd_status vd_stf(vd_handle h, uint32_t* passes) {
-  CHECK_HANDLE(h);
-  DeviceGuard guard(h->device);
-  for (auto& sh : h->shards) {  // init as JFA: all EMPTY, seed pixels hold themselves
-    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
-    vdk::fill_empty<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4);
-    vd_status st = after_launch(h, "fill_empty");
-    if (st) return st;
-  }
-  vd_status st = stamp_all(h, h->seeds);
-  if (st) return st;
-  uint32_t n = 0;
-  while (true) {  // "until the grid is fully flooded" (P:68): stop once no EMPTY is left
+  if (h->jfa_vn_waves > 0) {
+    if ((st = jfa_finish(h))) return st;
+    // dJFA needs a complete diagram: count what is still EMPTY (synchronises)
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
     for (auto& sh : h->shards) {
       const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
@@ -649,8 +665,33 @@ vd_status vd_stf(vd_handle h, uint32_t* passes) {
     }
     uint64_t empty = 0;
     if ((st = reduce_to_host(h, &empty))) return st;
+    h->has_diagram = empty == 0;
+    return VD_OK;
+  }
+  h->last_passes = (uint32_t)ks.size();
+  h->has_diagram = true;
+  return VD_OK;
+}
+
+vd_status vd_stf(vd_handle h, uint32_t* passes) {
+  CHECK_HANDLE(h);
+  DeviceGuard guard(h->device);
+  vd_status st = jfa_init(h);  // as JFA
+  if (st) return st;
+  const uint32_t u = unclaimed_label(h);
+  uint32_t n = 0;
+  while (true) {  // "until the grid is fully flooded" (P:68): stop once no EMPTY is left
+    CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+    for (auto& sh : h->shards) {
+      const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
+      vdk::count_value<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+                                                                  u, h->counter);
+      if ((st = after_launch(h, "count_value"))) return st;
+    }
+    uint64_t empty = 0;
+    if ((st = reduce_to_host(h, &empty))) return st;
     if (empty == 0) break;
-    if ((st = run_pass(h, 1, true))) return st;
+    if ((st = run_pass(h, 1, u == VD_EMPTY))) return st;
     ++n;
   }
   h->last_passes = n;

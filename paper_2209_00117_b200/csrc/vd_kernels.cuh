@@ -281,7 +281,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   if (tid == 0) {
     const int P = (int)a.pitch;
     for (int i = 0; i < nlist; ++i) {
-      int r = y0 + (i - 1) * k;
+      int r = y0 + (i - 1) * k;       // outside the grid: stage the centre row again
       if (r < 0) r += k;
       else if (r >= N) r -= k;
       const uint32_t* src = BANDED ? row_ptr(a, r) : a.in + (int64_t)(r - a.row0) * a.pitch;
@@ -417,10 +417,23 @@ __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
 // ------------------------------------------------------------------ JFA init
 // P:68 "defining the positions as the starting points for each flood": every pixel
 // EMPTY, then each seed pixel holds its own label.
-__global__ void fill_empty(uint4* __restrict__ p, int64_t n4) {
-  const uint4 v = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+__global__ void fill_value(uint4* __restrict__ p, int64_t n4, uint32_t value) {
+  const uint4 v = make_uint4(value, value, value, value);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
+}
+
+// After a JFA / StF that started from the virtual far seed V (vd.cu: jfa_init), turn the
+// V labels that survived (only possible with Von Neumann-only waves) back into EMPTY.
+__global__ void replace_value(uint4* __restrict__ p, int64_t n4, uint32_t from, uint32_t to) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    uint4 v = p[i];
+    v.x = v.x == from ? to : v.x;
+    v.y = v.y == from ? to : v.y;
+    v.z = v.z == from ? to : v.z;
+    v.w = v.w == from ? to : v.w;
+    p[i] = v;
+  }
 }
 
 // labels[seed pixel] <- seed label, for seeds whose row lies in [row0, row0 + rows).
