@@ -135,9 +135,11 @@ struct vd_ctx {
   bool has_diagram = false;
   uint32_t* seeds = nullptr;      // [s] current positions (labels)
   uint32_t* seeds_new = nullptr;  // [s] scratch for the move
-  short2* disp = nullptr;         // [s] displacements on device
-  short2* disp_stage = nullptr;   // [s] pinned host staging
-  cudaEvent_t disp_done = nullptr;
+  short2* disp_buf[2] = {nullptr, nullptr};  // [s] displacements on device, two slots
+  int disp_slot = 0;
+  cudaEvent_t disp_used[2] = {nullptr, nullptr};  // last kernel reading each slot done
+  cudaStream_t copy_stream = nullptr;             // host -> device uploads
+  cudaEvent_t copy_done = nullptr;
   uint32_t* fwd = nullptr;        // [N*N] forward map (dJFA), allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
   unsigned long long* counter_h = nullptr;   // pinned host copy
@@ -188,6 +190,9 @@ vd_status fail(vd_ctx* h, vd_status st, const char* fmt, ...) {
     if ((h)->sticky != VD_OK) return (h)->sticky; \
   } while (0)
 
+// Row-sweep kernels (remap, match_count, label_hash, count_value): CTAs stride over rows.
+int rows_grid(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(rows, 148 * 8)); }
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
@@ -206,19 +211,28 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// Copy s displacement pairs (host or device) to h->disp, asynchronously and safely: host
-// data goes through the handle's pinned staging buffer, so the caller may reuse its array
-// as soon as the call returns.
-vd_status upload_disp(vd_ctx* h, const int16_t* disp_xy) {
+// Bring s displacement pairs (host or device) into one of two device slots and return it.
+// Host data (pinned or pageable) is copied on a separate copy stream -- overlapping the
+// kernels still running on the handle's stream -- after the previous reader of that slot
+// (two calls ago) has finished; the call returns once the copy is complete (the caller may
+// reuse its array), and the handle's stream waits for it.  Device data is copied on the
+// handle's stream.  The caller records h->disp_used[slot] after the kernel reading it.
+vd_status upload_disp(vd_ctx* h, const int16_t* disp_xy, const short2** dev, int* slot_out) {
   const size_t bytes = h->s * sizeof(short2);
+  const int slot = h->disp_slot;
+  h->disp_slot ^= 1;
+  short2* dst = h->disp_buf[slot];
   if (is_device_ptr(disp_xy)) {
-    CK(cudaMemcpyAsync(h->disp, disp_xy, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(dst, disp_xy, bytes, cudaMemcpyDeviceToDevice, h->stream));
   } else {
-    CK(cudaEventSynchronize(h->disp_done));  // previous upload out of the staging buffer
-    memcpy(h->disp_stage, disp_xy, bytes);
-    CK(cudaMemcpyAsync(h->disp, h->disp_stage, bytes, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaEventRecord(h->disp_done, h->stream));
+    CK(cudaStreamWaitEvent(h->copy_stream, h->disp_used[slot], 0));
+    CK(cudaMemcpyAsync(dst, disp_xy, bytes, cudaMemcpyHostToDevice, h->copy_stream));
+    CK(cudaEventRecord(h->copy_done, h->copy_stream));
+    CK(cudaEventSynchronize(h->copy_done));
+    CK(cudaStreamWaitEvent(h->stream, h->copy_done, 0));
   }
+  *dev = dst;
+  *slot_out = slot;
   return VD_OK;
 }
 
@@ -368,11 +382,15 @@ vd_status stamp_all(vd_ctx* h, const uint32_t* seeds) {
 }
 
 vd_status move_seeds(vd_ctx* h, const int16_t* disp_xy) {
-  vd_status st = upload_disp(h, disp_xy);
+  const short2* d;
+  int slot;
+  vd_status st = upload_disp(h, disp_xy, &d, &slot);
   if (st) return st;
-  vdk::move_clamp<<<grid_for((int64_t)h->s, 256), 256, 0, h->stream>>>(h->seeds, h->disp, h->seeds_new,
-                                                                       (int64_t)h->s, (int)h->N);
-  return after_launch(h, "move_clamp");
+  vdk::move_clamp<<<grid_for((int64_t)h->s, 256), 256, 0, h->stream>>>(h->seeds, d, h->seeds_new, (int64_t)h->s,
+                                                                       (int)h->N);
+  if ((st = after_launch(h, "move_clamp"))) return st;
+  CK(cudaEventRecord(h->disp_used[slot], h->stream));
+  return VD_OK;
 }
 
 vd_status reduce_to_host(vd_ctx* h, uint64_t* out) {
@@ -407,12 +425,16 @@ void free_all(vd_ctx* h) {
   h->shards.clear();
   cudaFree(h->seeds);
   cudaFree(h->seeds_new);
-  cudaFree(h->disp);
+  cudaFree(h->disp_buf[0]);
+  cudaFree(h->disp_buf[1]);
   cudaFree(h->fwd);
   cudaFree(h->counter);
-  if (h->disp_stage) cudaFreeHost(h->disp_stage);
+
   if (h->counter_h) cudaFreeHost(h->counter_h);
-  if (h->disp_done) cudaEventDestroy(h->disp_done);
+  for (auto e : h->disp_used)
+    if (e) cudaEventDestroy(e);
+  if (h->copy_done) cudaEventDestroy(h->copy_done);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (auto e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
   if (h->comm && g_nccl.ok) g_nccl.CommDestroy(h->comm);
@@ -611,12 +633,16 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   }
   CKC(cudaMalloc(&h->seeds, s * sizeof(uint32_t)));
   CKC(cudaMalloc(&h->seeds_new, s * sizeof(uint32_t)));
-  CKC(cudaMalloc(&h->disp, s * sizeof(short2)));
-  CKC(cudaMallocHost(&h->disp_stage, s * sizeof(short2)));
+  CKC(cudaMalloc(&h->disp_buf[0], s * sizeof(short2)));
+  CKC(cudaMalloc(&h->disp_buf[1], s * sizeof(short2)));
+  CKC(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&h->copy_done, cudaEventDisableTiming));
+  for (auto& e : h->disp_used) {
+    CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CKC(cudaEventRecord(e, h->stream));
+  }
   CKC(cudaMalloc(&h->counter, sizeof(unsigned long long)));
   CKC(cudaMallocHost(&h->counter_h, sizeof(unsigned long long)));
-  CKC(cudaEventCreateWithFlags(&h->disp_done, cudaEventDisableTiming));
-  CKC(cudaEventRecord(h->disp_done, h->stream));
   CKC(cudaMemcpyAsync(h->seeds, packed.data(), s * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
   CKC(cudaStreamSynchronize(h->stream));
   if (cfg.world > 1) {
@@ -658,8 +684,7 @@ vd_status vd_jfa(vd_handle h) {
     // dJFA needs a complete diagram: count what is still EMPTY (synchronises)
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
     for (auto& sh : h->shards) {
-      const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
-      vdk::count_value<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+      vdk::count_value<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
                                                                   VD_EMPTY, h->counter);
       if ((st = after_launch(h, "count_value"))) return st;
     }
@@ -683,8 +708,7 @@ vd_status vd_stf(vd_handle h, uint32_t* passes) {
   while (true) {  // "until the grid is fully flooded": stop once no EMPTY is left
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
     for (auto& sh : h->shards) {
-      const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
-      vdk::count_value<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+      vdk::count_value<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
                                                                   u, h->counter);
       if ((st = after_launch(h, "count_value"))) return st;
     }
@@ -722,16 +746,18 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   }
   std::vector<uint32_t> ks;
   schedule_djfa(h->N, h->s, d_max, h->extras, ks);
-  vd_status st = upload_disp(h, disp_xy);
+  const short2* dd;
+  int slot;
+  vd_status st = upload_disp(h, disp_xy, &dd, &slot);
   if (st) return st;
   const int gs = grid_for((int64_t)h->s, 256);
   // 1. SimulateParticles + forward map old -> new (R-9); fwd is all EMPTY on entry
-  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, h->disp, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N);
+  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N);
   if ((st = after_launch(h, "move_fwd"))) return st;
+  CK(cudaEventRecord(h->disp_used[slot], h->stream));
   // 2. labels follow their seeds (reuse of VD_{t-1})
   for (auto& sh : h->shards) {
-    const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
-    vdk::remap<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd);
+    vdk::remap<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd);
     if ((st = after_launch(h, "remap"))) return st;
   }
   // 3. re-stamp the new seed pixels; fwd back to all-EMPTY
@@ -800,8 +826,7 @@ vd_status vd_similarity(vd_handle h, vd_handle ref, double* pct, uint64_t* match
   for (size_t g = 0; g < h->shards.size(); ++g) {
     const Shard& a = h->shards[g];
     const Shard& b = ref->shards[g];
-    const int64_t work = (int64_t)a.rows * ((h->N + 3) / 4);
-    vdk::match_count<<<grid_for(work, 256), 256, 0, h->stream>>>(a.buf[h->cur], b.buf[ref->cur], h->pitch,
+    vdk::match_count<<<rows_grid(a.rows), 256, 0, h->stream>>>(a.buf[h->cur], b.buf[ref->cur], h->pitch,
                                                                 (int)a.rows, (int)h->N, h->counter);
     vd_status st = after_launch(h, "match_count");
     if (st) return st;
@@ -825,8 +850,7 @@ vd_status vd_similarity_host(vd_handle h, const uint32_t* ref_labels, double* pc
     uint32_t* scratch = sh.buf[h->cur ^ 1];
     CK(cudaMemcpy2DAsync(scratch, h->pitch * sizeof(uint32_t), ref_labels + off_rows * h->N, h->N * sizeof(uint32_t),
                          h->N * sizeof(uint32_t), sh.rows, cudaMemcpyDefault, h->stream));
-    const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
-    vdk::match_count<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], scratch, h->pitch, (int)sh.rows,
+    vdk::match_count<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], scratch, h->pitch, (int)sh.rows,
                                                                 (int)h->N, h->counter);
     vd_status st = after_launch(h, "match_count");
     if (st) return st;
@@ -846,8 +870,7 @@ vd_status vd_label_hash(vd_handle h, uint64_t* out) {
   DeviceGuard guard(h->device);
   CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
   for (auto& sh : h->shards) {
-    const int64_t work = (int64_t)sh.rows * ((h->N + 3) / 4);
-    vdk::label_hash<<<grid_for(work, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
+    vdk::label_hash<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
                                                                (int)sh.rows, (int)h->N, h->counter);
     vd_status st = after_launch(h, "label_hash");
     if (st) return st;

@@ -501,21 +501,23 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
 
 // Reuse VD_{t-1}: every label moves with its seed, labels[p] <- fwd[labels[p]].
 // Neighbouring pixels mostly share a label, so the gathers hit L1.
+// Row-major sweeps below: CTAs stride over rows, threads over 4-label quads of a row, with
+// the quad loop unrolled so that several 128-bit loads are in flight per thread.
 __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd) {
-  const int xq = (N + 3) / 4;
-  const int64_t total = (int64_t)rows * xq;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / xq;
-    int x = (int)(i - r * xq) * 4;
-    uint4* p = reinterpret_cast<uint4*>(g + r * pitch + x);
-    uint4 v = *p;
-    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    uint32_t* row = g + (int64_t)r * pitch;
+#pragma unroll 4
+    for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
+      uint4* p = reinterpret_cast<uint4*>(row + x);
+      uint4 v = *p;
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t c = w[e];
-      if (x + e < N && c != EMPTY) w[e] = __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu));
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t c = w[e];
+        if (x + e < N && c != EMPTY) w[e] = __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu));
+      }
+      *p = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    *p = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -539,33 +541,34 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
 // Eq. 5 numerator: count of pixels with equal labels in a band.
 __global__ void match_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t pitch,
                             int rows, int N, unsigned long long* __restrict__ out) {
-  const int xq = (N + 3) / 4;
-  const int64_t total = (int64_t)rows * xq;
-  uint64_t cnt = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / xq;
-    int x = (int)(i - r * xq) * 4;
-    uint4 u = __ldg(reinterpret_cast<const uint4*>(a + r * pitch + x));
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(b + r * pitch + x));
-    int nv = min(4, N - x);
-    cnt += (u.x == v.x) + (nv > 1 && u.y == v.y) + (nv > 2 && u.z == v.z) + (nv > 3 && u.w == v.w);
+  uint32_t cnt = 0;  // per thread: at most rows/gridDim * N/blockDim*... < 2^32 for any grid we allow
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint32_t* ra = a + (int64_t)r * pitch;
+    const uint32_t* rb = b + (int64_t)r * pitch;
+#pragma unroll 4
+    for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(ra + x));
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(rb + x));
+      const int nv = min(4, N - x);
+      cnt += (u.x == v.x) + (nv > 1 && u.y == v.y) + (nv > 2 && u.z == v.z) + (nv > 3 && u.w == v.w);
+    }
   }
   uint64_t t = block_sum_u64(cnt);
   if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
 }
 
-// Number of pixels of a band holding `value` (StF's "fully flooded" test with EMPTY).
+// Number of pixels of a band holding `value` (StF's "fully flooded" test).
 __global__ void count_value(const uint32_t* __restrict__ g, int64_t pitch, int rows, int N, uint32_t value,
                             unsigned long long* __restrict__ out) {
-  const int xq = (N + 3) / 4;
-  const int64_t total = (int64_t)rows * xq;
-  uint64_t cnt = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / xq;
-    int x = (int)(i - r * xq) * 4;
-    uint4 u = __ldg(reinterpret_cast<const uint4*>(g + r * pitch + x));
-    int nv = min(4, N - x);
-    cnt += (u.x == value) + (nv > 1 && u.y == value) + (nv > 2 && u.z == value) + (nv > 3 && u.w == value);
+  uint32_t cnt = 0;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint32_t* row = g + (int64_t)r * pitch;
+#pragma unroll 4
+    for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + x));
+      const int nv = min(4, N - x);
+      cnt += (u.x == value) + (nv > 1 && u.y == value) + (nv > 2 && u.z == value) + (nv > 3 && u.w == value);
+    }
   }
   uint64_t t = block_sum_u64(cnt);
   if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
@@ -581,18 +584,18 @@ __device__ __forceinline__ uint64_t smix(uint64_t z) {
 // Checksum sum_p splitmix64((p << 32) | label[p]) over a band (p = global y*N + x).
 __global__ void label_hash(const uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N,
                            unsigned long long* __restrict__ out) {
-  const int xq = (N + 3) / 4;
-  const int64_t total = (int64_t)rows * xq;
   uint64_t h = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / xq;
-    int x = (int)(i - r * xq) * 4;
-    uint4 u = __ldg(reinterpret_cast<const uint4*>(g + r * pitch + x));
-    uint32_t w[4] = {u.x, u.y, u.z, u.w};
-    uint64_t p = (uint64_t)(row0 + r) * (uint64_t)N + (uint64_t)x;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint32_t* row = g + (int64_t)r * pitch;
+    const uint64_t p0 = (uint64_t)(row0 + r) * (uint64_t)N;
+#pragma unroll 4
+    for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + x));
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (x + e < N) h += smix(((p + e) << 32) | w[e]);
+      for (int e = 0; e < 4; ++e)
+        if (x + e < N) h += smix(((p0 + x + e) << 32) | w[e]);
+    }
   }
   uint64_t t = block_sum_u64(h);
   if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)t);
