@@ -115,10 +115,10 @@ __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t 
 // ---- shared-memory row staging with cp.async.bulk (TMA bulk copies) -----------------
 constexpr int kW = kVec * kThreads;      // columns per CTA (512)
 #ifndef VD_MAX_WALK
-#define VD_MAX_WALK 16
+#define VD_MAX_WALK 24
 #endif
 #ifndef VD_SMEM_KB
-#define VD_SMEM_KB 48
+#define VD_SMEM_KB 56
 #endif
 constexpr int kMaxWalk = VD_MAX_WALK;    // output rows per walk (upper bound)
 constexpr int kSmemBudget = VD_SMEM_KB * 1024;  // staged rows per CTA
@@ -278,9 +278,9 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   if (tid < nlist) mbar_init(&bars[tid], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();  // barrier initialisation visible to every thread (and to the async proxy)
-  if (tid == 0) {
+  if ((tid & 31) == 0) {  // lane 0 of each warp issues every kThreads/32-th row, in row order
     const int P = (int)a.pitch;
-    for (int i = 0; i < nlist; ++i) {
+    for (int i = tid >> 5; i < nlist; i += kThreads / 32) {
       int r = y0 + (i - 1) * k;       // outside the grid: stage the centre row again
       if (r < 0) r += k;
       else if (r >= N) r -= k;
