@@ -157,8 +157,9 @@ vd_status vd_similarity_host(vd_handle h, const uint32_t* ref_labels, double* pc
                              uint64_t* matches);
 
 /* Order-independent checksum of the current diagram: sum over pixels p = y*N + x of
- * splitmix64((p << 32) | label[p]) mod 2^64 (summed over ranks when world > 1).  Reads
- * the whole diagram once and returns 8 bytes; used as the per-step result read-back. */
+ * fmix32((uint32)(p * 0x9E3779B9) ^ label[p]) in uint64 (fmix32 = MurmurHash3's 32-bit
+ * finaliser; summed over ranks when world > 1).  Reads the whole diagram once and returns
+ * 8 bytes; used as the per-step result read-back. */
 vd_status vd_label_hash(vd_handle h, uint64_t* out);
 
 /* Copy the diagram to host: N*N labels (world = 1, any virtual_shards), or this rank's

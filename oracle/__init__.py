@@ -225,7 +225,7 @@ def similarity(a: np.ndarray, b: np.ndarray) -> float:
 
 
 def label_hash(G: np.ndarray) -> int:
-    """Order-independent u64 checksum: sum_p splitmix64((p << 32) | label[p])."""
+    """Order-independent u64 checksum: sum_p fmix32((uint32)(p * 0x9E3779B9) ^ label[p])."""
     G = np.ascontiguousarray(G, dtype=np.uint32)
     return int(_load().or_label_hash(G.size, _ptr(G)))
 

@@ -376,16 +376,19 @@ uint64_t or_match_count(uint64_t np, const uint32_t* a, const uint32_t* b) {
 }
 
 /* Order-independent checksum of a label map (not from the paper; used to compare whole
- * diagrams by one number): sum over p of splitmix64((p << 32) | label[p]) mod 2^64. */
-static uint64_t smix(uint64_t z) {
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
+ * diagrams by one number): sum over p of fmix32((uint32)(p * 0x9E3779B9) ^ label[p])
+ * in uint64, with fmix32 the MurmurHash3 32-bit finaliser. */
+static uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
 }
 uint64_t or_label_hash(uint64_t np, const uint32_t* g) {
     uint64_t h = 0;
-    for (uint64_t p = 0; p < np; p++) h += smix((p << 32) | g[p]);
+    for (uint64_t p = 0; p < np; p++) h += fmix32((uint32_t)(p * 0x9E3779B9u) ^ g[p]);
     return h;
 }
 

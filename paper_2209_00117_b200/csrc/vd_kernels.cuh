@@ -574,27 +574,36 @@ __global__ void count_value(const uint32_t* __restrict__ g, int64_t pitch, int r
   if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
 }
 
-__device__ __forceinline__ uint64_t smix(uint64_t z) {
-  z += 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
 }
 
-// Checksum sum_p splitmix64((p << 32) | label[p]) over a band (p = global y*N + x).
+// Checksum sum_p fmix32((uint32)(p * 0x9E3779B9) ^ label[p]) in uint64 over a band
+// (p = global y*N + x < 2^32).
 __global__ void label_hash(const uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N,
                            unsigned long long* __restrict__ out) {
   uint64_t h = 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const uint32_t* row = g + (int64_t)r * pitch;
-    const uint64_t p0 = (uint64_t)(row0 + r) * (uint64_t)N;
+    const uint32_t p0 = (uint32_t)(row0 + r) * (uint32_t)N;
 #pragma unroll 4
     for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + x));
       const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      uint32_t acc = 0, carry = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (x + e < N) h += smix(((p0 + x + e) << 32) | w[e]);
+        if (x + e < N) {
+          const uint32_t m = fmix32((p0 + (uint32_t)(x + e)) * 0x9E3779B9u ^ w[e]);
+          acc += m;
+          carry += acc < m;
+        }
+      h += ((uint64_t)carry << 32) | acc;
     }
   }
   uint64_t t = block_sum_u64(h);

@@ -34,7 +34,14 @@ def test_label_hash_order_independent_and_sensitive():
     H = G.copy()
     H[5, 5] ^= 1
     assert oracle.label_hash(H) != h
-    # closed form on a tiny map: sum of splitmix64((p << 32) | label) mod 2^64
+    # closed form on a tiny map: MurmurHash3's fmix32 reference vectors, then the sum
+    def fmix32(h):
+        h ^= h >> 16
+        h = (h * 0x85EBCA6B) & 0xFFFFFFFF
+        h ^= h >> 13
+        h = (h * 0xC2B2AE35) & 0xFFFFFFFF
+        return h ^ (h >> 16)
+    assert fmix32(0) == 0 and fmix32(1) == 0x514E28B7  # smhasher's fmix32(1)
     g = np.array([[7, 9]], dtype=np.uint32)
-    z = synth.splitmix64(np.array([(0 << 32) | 7, (1 << 32) | 9], dtype=np.uint64))
-    assert oracle.label_hash(g) == int(z.sum(dtype=np.uint64))
+    want = fmix32((0 * 0x9E3779B9) & 0xFFFFFFFF ^ 7) + fmix32((1 * 0x9E3779B9) & 0xFFFFFFFF ^ 9)
+    assert oracle.label_hash(g) == want
