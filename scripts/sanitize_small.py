@@ -1,16 +1,30 @@
-"""Small JFA + dJFA run for compute-sanitizer (no oracle needed)."""
+"""Small JFA / dJFA / StF / variant runs for compute-sanitizer (no oracle needed)."""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
 import synth  # noqa: E402
 import paper_2209_00117_b200 as vd  # noqa: E402
 
-for N, s, G in ((64, 16, 0), (1024, 1024, 0), (1031, 200, 0), (256, 100, 4)):
+cases = [
+    (64, 16, {}), (1031, 200, {}), (1024, 1024, {}), (256, 100, {"virtual_shards": 4}),
+    (300, 50, {"metric": "manhattan", "vn_waves": 2}), (128, 30, {"jfa_vn_waves": 99}),
+]
+for N, s, cfg in cases:
     xy = synth.uniform_seeds(N, s, rng_seed=1)
-    d = vd.VoronoiDiagram(N, xy, virtual_shards=G)
+    d = vd.VoronoiDiagram(N, xy, **cfg)
     d.jfa()
     for f in range(2):
-        d.djfa_step(synth.displacements(s, 2, f, rng_seed=1), 2)
-    print(N, s, G, hex(d.label_hash()), flush=True)
+        try:
+            d.djfa_step(synth.displacements(s, 2, f, rng_seed=1), 2)
+        except vd.VDError:
+            pass  # Von Neumann-only JFA may be incomplete: dJFA is refused (VD_ERR_STATE)
+    e = vd.VoronoiDiagram(N, xy, **{k: v for k, v in cfg.items() if k != "jfa_vn_waves"})
+    e.stf()
+    e.set_labels(d.labels())
+    e.jump_pass(3)
+    print(N, s, cfg, hex(d.label_hash()), d.match_count(d), flush=True)
     d.close()
+    e.close()
