@@ -143,7 +143,9 @@ vd_status vd_set_labels(vd_handle h, const uint32_t* labels);
  * wave, in gather form R-12), including the halo exchange when sharded, with
  * the handle's metric.  flags: VD_PASS_VON_NEUMANN = only the 4 axis neighbours
  * (P:154-160), else the Moore 8 of Table 1.  Powers of two use the fast kernel; any
- * other k the generic one (same results). */
+ * other k the generic one (same results).  On a handle holding a diagram (no EMPTY, as
+ * after vd_jfa / vd_djfa_step / a complete vd_set_labels, world == 1) the EMPTY-free
+ * kernels run, including the windowed one for 32768 < N <= 65536, k <= 4096. */
 vd_status vd_pass(vd_handle h, uint32_t k, uint32_t flags);
 
 /* Eq. 5: 100 * matching pixels / total pixels between the diagrams of h and

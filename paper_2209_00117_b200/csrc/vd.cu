@@ -257,31 +257,42 @@ vd_status timed_end(vd_ctx* h, uint64_t px) {
 
 // Which kernel variant can take this pass exactly (see vd_kernels.cuh).
 // Launch one fast-pass instantiation; each opts into the largest staging size once.
-template <int KM, bool ME, bool BD, int MT, bool VN>
+template <int KM, bool ME, bool BD, int MT, bool VN, bool REL>
 cudaError_t launch_fast(const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
   static cudaError_t attr = cudaErrorNotReady;
   if (attr == cudaErrorNotReady)
-    attr = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                vdk::kSmemBudget);
+    attr = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, vdk::kSmemBudget);
   if (attr != cudaSuccess) return attr;
-  vdk::jump_pass_fast<KM, ME, BD, MT, VN><<<grid, blk, sm, st>>>(a);
+  vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL><<<grid, blk, sm, st>>>(a);
   return cudaSuccess;
 }
-template <int KM, bool ME, bool BD>
+template <int KM, bool ME, bool BD, bool REL>
 cudaError_t launch_fast_mv(int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
-  if (metric == 0) return vn ? launch_fast<KM, ME, BD, 0, true>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 0, false>(a, g, b, sm, st);
-  return vn ? launch_fast<KM, ME, BD, 1, true>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 1, false>(a, g, b, sm, st);
+  if (metric == 0)
+    return vn ? launch_fast<KM, ME, BD, 0, true, REL>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 0, false, REL>(a, g, b, sm, st);
+  return vn ? launch_fast<KM, ME, BD, 1, true, REL>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 1, false, REL>(a, g, b, sm, st);
 }
 template <int KM>
-cudaError_t launch_fast_k(bool me, bool bd, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm,
-                          cudaStream_t st) {
-  if (me) return bd ? launch_fast_mv<KM, true, true>(metric, vn, a, g, b, sm, st)
-                    : launch_fast_mv<KM, true, false>(metric, vn, a, g, b, sm, st);
-  return bd ? launch_fast_mv<KM, false, true>(metric, vn, a, g, b, sm, st)
-            : launch_fast_mv<KM, false, false>(metric, vn, a, g, b, sm, st);
+cudaError_t launch_fast_k(bool me, bool bd, bool rel, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b,
+                          size_t sm, cudaStream_t st) {
+  if (rel) {  // windowed coordinates (grids beyond the plain fast kernel's range)
+    if (me) return bd ? launch_fast_mv<KM, true, true, true>(metric, vn, a, g, b, sm, st)
+                      : launch_fast_mv<KM, true, false, true>(metric, vn, a, g, b, sm, st);
+    return bd ? launch_fast_mv<KM, false, true, true>(metric, vn, a, g, b, sm, st)
+              : launch_fast_mv<KM, false, false, true>(metric, vn, a, g, b, sm, st);
+  }
+  if (me) return bd ? launch_fast_mv<KM, true, true, false>(metric, vn, a, g, b, sm, st)
+                    : launch_fast_mv<KM, true, false, false>(metric, vn, a, g, b, sm, st);
+  return bd ? launch_fast_mv<KM, false, true, false>(metric, vn, a, g, b, sm, st)
+            : launch_fast_mv<KM, false, false, false>(metric, vn, a, g, b, sm, st);
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
+// Windowed fast pass (REL) for the grids beyond fast_ok (N > 32768; N > 16384 when EMPTY may
+// occur), for steps small enough that a walk and its neighbour rows fit the 32768-wide window
+// (dJFA's delta passes, JFA's last 13).  Walks meeting EMPTY or far labels are recomputed exactly.
+bool rel_ok(uint32_t N, bool may_empty, uint32_t k) { return !fast_ok(N, may_empty) && k <= 4096; }
 
 vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn) {
   vdk::PassArgs a;
@@ -307,19 +318,21 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn)
   a.vn = vn ? 1 : 0;
   vd_status st = timed_begin(h);
   if (st) return st;
-  if (fast_ok(h->N, may_empty) && (k & (k - 1)) == 0) {
+  const bool rel = rel_ok(h->N, may_empty, k);
+  if ((fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, B);
     const uint32_t per_res = (B + k - 1) / k;
     a.walk = vdk::walk_len((int)k);
+    if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
     const bool banded = sh.top != nullptr;
     const size_t sm = vdk::pass_smem((int)k);
     cudaError_t e;
-    if (k == 1) e = launch_fast_k<1>(may_empty, banded, h->metric, vn, a, grid, blk, sm, h->stream);
-    else if (k == 2) e = launch_fast_k<2>(may_empty, banded, h->metric, vn, a, grid, blk, sm, h->stream);
-    else e = launch_fast_k<4>(may_empty, banded, h->metric, vn, a, grid, blk, sm, h->stream);
+    if (k == 1) e = launch_fast_k<1>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    else if (k == 2) e = launch_fast_k<2>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    else e = launch_fast_k<4>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     CK(e);
   } else {
     a.segs = 1;
@@ -810,7 +823,10 @@ vd_status vd_pass(vd_handle h, uint32_t k, uint32_t flags) {
     if (k > B && k % B != 0) return fail(h, VD_ERR_ARG, "sharded pass needs k < band rows or a multiple of them");
     if (k > h->hcap && k < B) return fail(h, VD_ERR_ARG, "halo capacity exceeded");
   }
-  return run_pass(h, k, true, (flags & VD_PASS_VON_NEUMANN) != 0);
+  // A complete map (no EMPTY, known on every shard of this handle) stays complete under a
+  // pass, so the EMPTY-free kernels apply; across ranks completeness is not known globally.
+  const bool may_empty = !h->has_diagram || h->world > 1;
+  return run_pass(h, k, may_empty, (flags & VD_PASS_VON_NEUMANN) != 0);
 }
 
 vd_status vd_similarity(vd_handle h, vd_handle ref, double* pct, uint64_t* matches) {

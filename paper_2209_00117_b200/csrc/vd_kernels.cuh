@@ -177,9 +177,14 @@ __device__ __forceinline__ void unpack(const uint4& v, uint32_t* w) { w[0] = v.x
 // centre / right vectors in the stage.  KM = min(k, kVec): KM == kVec means the neighbour
 // vectors at x -+ k are aligned; KM < kVec takes the neighbours from the adjacent vectors.
 // METRIC 0: Euclidean (q = cy^2 + dx^2); METRIC 1: Manhattan, dJFAm (q = |dx|).
-template <int KM, bool MAY_EMPTY, bool FIX, int METRIC>
+// REL (grids wider than 32768): labels are first moved into the CTA's 32768-wide window,
+// c' = (cy - oy, cx - ox) as two 16-bit lanes (nbase2 = -(oy, ox)); a label outside the
+// window sets bit 15 of a lane, which `bad` accumulates (the walk is then recomputed
+// exactly).  xr = x - ox is the thread's column in the window.
+template <int KM, bool MAY_EMPTY, bool FIX, int METRIC, bool REL = false>
 __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, int li, int ci, int ri, int x, int k,
-                                              int N, uint32_t vempty, uint32_t sh16, const int (&xs16)[kVec], Row& R) {
+                                              int N, uint32_t vempty, uint32_t sh16, const int (&xs16)[kVec], Row& R,
+                                              uint32_t nbase2 = 0, uint32_t* bad = nullptr, int xr = 0) {
   using V = typename VecT<kVec>::T;
   uint32_t w[3 * kVec];
   unpack(*reinterpret_cast<const V*>(st + li), w);
@@ -201,14 +206,20 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
 #pragma unroll
   for (int i = 0; i < 3 * kVec; ++i) {
     uint32_t c = R.c[i];
-    if (MAY_EMPTY) { c = __vminu2(c, vempty); R.c[i] = c; }  // EMPTY -> virtual far seed
+    if (MAY_EMPTY && !REL) { c = __vminu2(c, vempty); R.c[i] = c; }  // EMPTY -> virtual far seed
+    if constexpr (REL) {  // window coordinates; EMPTY (MAY_EMPTY) also sends the walk to the exact path
+      if (MAY_EMPTY && c == EMPTY) *bad |= 0x8000u;
+      c = __vadd2(c, nbase2);
+      R.c[i] = c;
+      *bad |= c;
+    }
     const int cy = (int)(c >> 16);
     R.cy[i] = cy;
     if constexpr (METRIC == 0) {
       const int D = (int)(c * sh16) + xs16[i % kVec];         // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
       R.q[i] = cy * cy + __mulhi(D, D);                        // cy^2 + dx^2
     } else {
-      R.q[i] = (int)__sad((int)(c & 0xFFFFu), x + (i % kVec), 0u);  // |cx - (x+e)|
+      R.q[i] = (int)__sad((int)(c & 0xFFFFu), (REL ? xr : x) + (i % kVec), 0u);  // |cx - (x+e)|
     }
   }
 }
@@ -253,6 +264,15 @@ __device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Ro
                            __vimin3_u32(w[6], w[7], w[8]));
 }
 
+// Exact (64-bit) candidate test: key (distance, label), EMPTY = +infinity.
+__device__ __forceinline__ void consider_wide(uint32_t c, int x, int y, int metric, uint64_t& bd, uint32_t& bc) {
+  if (c == EMPTY) return;
+  int64_t dx = (int64_t)(c & 0xFFFFu) - x, dy = (int64_t)(c >> 16) - y;
+  uint64_t d = metric == 0 ? (uint64_t)(dx * dx) + (uint64_t)(dy * dy)
+                           : (uint64_t)(dx < 0 ? -dx : dx) + (uint64_t)(dy < 0 ? -dy : dy);
+  if (d < bd || (d == bd && c < bc)) { bd = d; bc = c; }
+}
+
 // One CTA = 512 columns x one walk (up to kMaxWalk output rows of one residue class
 // y0, y0+k, ...).  At entry, thread 0 stages ALL of the walk's input rows
 // y0-k, y0, ..., y_last+k into shared memory with cp.async.bulk, one mbarrier per row;
@@ -262,7 +282,7 @@ __device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Ro
 // the centre row (the producer stages that row again), columns outside the grid by the
 // pixel's own column: duplicates never change a minimum.
 // BANDED: rows beyond the band come from the halo buffers (row_ptr).
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, int METRIC, bool VN>
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, int METRIC, bool VN, bool REL>
 __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t* smem) {
   const int k = a.k, N = a.N;
   const int tid = (int)threadIdx.x;
@@ -309,14 +329,27 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   const int li = (x - nstep >= 0) ? (spans3 ? kVec * tid : ci - nstep) : ci;
   const int ri = (x + nstep < N) ? (spans3 ? 2 * kW + kVec * tid : ci + nstep) : ci;
   const uint32_t sh16 = a.sh16;  // 65536, from memory so ptxas keeps the multiply on the FMA pipe
+  // REL: the window origin (ox, oy) in [0, max(N-32768, 0)]^2, centred on the walk where the
+  // grid allows, so that a label outside the window always sets bit 15 of a 16-bit lane
+  // after the subtraction.
+  int ox = 0, oy = 0;
+  if constexpr (REL) {
+    const int omax = max(N - 32768, 0);  // window kept inside the grid
+    ox = min(max(x0 + kW / 2 - 16384, 0), omax);
+    oy = min(max(y0 + ((nout - 1) * k) / 2 - 16384, 0), omax);
+  }
+  const uint32_t base2 = ((uint32_t)oy << 16) | (uint32_t)ox;
+  const uint32_t nbase2 = __vsub2(0u, base2);
+  uint32_t bad = 0;
   int xs16[kVec];
 #pragma unroll
-  for (int e = 0; e < kVec; ++e) xs16[e] = -((x + e) << 16);
+  for (int e = 0; e < kVec; ++e) xs16[e] = -((x - ox + e) << 16);
   const bool active = x < N;
 
   auto consume = [&](int i, Row& R) {
     mbar_wait(&bars[i], 0u);
-    row_from_smem<KM, MAY_EMPTY, FIX, METRIC>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16, R);
+    row_from_smem<KM, MAY_EMPTY, FIX, METRIC, REL>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16,
+                                                   R, nbase2, &bad, x - ox);
   };
 
   Row r0, r1, r2;
@@ -333,8 +366,9 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     uint32_t o[kVec];
 #pragma unroll
     for (int e = 0; e < kVec; ++e) {
-      uint32_t v = best_of<METRIC, VN>(P, C, Nx, e, y);
-      if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
+      uint32_t v = best_of<METRIC, VN>(P, C, Nx, e, y - oy);
+      if (MAY_EMPTY && !REL) v = (v == a.vempty) ? EMPTY : v;
+      if (REL) v = __vadd2(v, base2);  // back to absolute coordinates
       o[e] = v;
     }
     if (active) {
@@ -351,9 +385,44 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     if (!step(r1, r2, r0)) break;
     if (!step(r2, r0, r1)) break;
   }
+  if constexpr (REL) {
+    // Some label of this walk lay outside the window: redo the walk exactly (64-bit keys)
+    // from the staged rows, which are still in shared memory.  Never happens for a
+    // converged dJFA diagram with dense seeds; keeps every grid exact.
+    if (__syncthreads_or((bad & 0x80008000u) != 0u)) {
+      for (int jj = 0; jj < nout; ++jj) {
+        const int yy = y0 + jj * k;
+        uint32_t o[kVec];
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          const int xe = x + e;
+          uint64_t bd = ~0ull;
+          uint32_t bc = EMPTY;
+          for (int rr = -1; rr <= 1; ++rr) {
+            const int r = yy + rr * k;
+            if (r < 0 || r >= N) continue;
+            const uint32_t* st = smem + (size_t)(jj + 1 + rr) * SE;
+            for (int cc = -1; cc <= 1; ++cc) {
+              if (VN && rr != 0 && cc != 0) continue;
+              const int q = xe + cc * k;
+              if (q < 0 || q >= N || xe >= N) continue;
+              const int off = spans3 ? (cc + 1) * kW + (q - (x0 + cc * k)) : q - (x0 - K4);
+              consider_wide(st[off], xe, yy, METRIC, bd, bc);
+            }
+          }
+          o[e] = bc;
+        }
+        if (active) {
+          uint32_t* pw = a.out + (int64_t)(yy - a.row0) * a.pitch + x;
+          if constexpr (kVec == 4) *reinterpret_cast<uint4*>(pw) = make_uint4(o[0], o[1], o[2], o[3]);
+          else *reinterpret_cast<uint2*>(pw) = make_uint2(o[0], o[1]);
+        }
+      }
+    }
+  }
 }
 
-template <int KM, bool MAY_EMPTY, bool BANDED, int METRIC = 0, bool VN = false>
+template <int KM, bool MAY_EMPTY, bool BANDED, int METRIC = 0, bool VN = false, bool REL = false>
 __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
@@ -368,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
   // is exact as a centre-vector substitution.
   const int nstep = KM >= kVec ? a.k : kVec;
   const bool fix = (KM < kVec || (a.N & (kVec - 1))) && (x0 < nstep + kVec || x0 + kW + nstep + kVec > a.N);
-  if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN>(a, x0, y0, dyn_smem);
-  else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN>(a, x0, y0, dyn_smem);
+  if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN, REL>(a, x0, y0, dyn_smem);
+  else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN, REL>(a, x0, y0, dyn_smem);
 }
 
 // ------------------------------------------------------------------ wide jump pass
@@ -377,14 +446,6 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
 // Same pass for grids the fast kernel cannot take exactly (N > 32768, or EMPTY present
 // with N > 23170): uint64 squared distances, explicit EMPTY, lexicographic (d2, label).
 // One thread per 4 adjacent pixels of one row, nine 128-bit loads.
-__device__ __forceinline__ void consider_wide(uint32_t c, int x, int y, int metric, uint64_t& bd, uint32_t& bc) {
-  if (c == EMPTY) return;
-  int64_t dx = (int64_t)(c & 0xFFFFu) - x, dy = (int64_t)(c >> 16) - y;
-  uint64_t d = metric == 0 ? (uint64_t)(dx * dx) + (uint64_t)(dy * dy)
-                           : (uint64_t)(dx < 0 ? -dx : dx) + (uint64_t)(dy < 0 ? -dy : dy);
-  if (d < bd || (d == bd && c < bc)) { bd = d; bc = c; }
-}
-
 __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
   const int yl = (int)(blockIdx.x / (unsigned)a.xblocks);

@@ -334,3 +334,90 @@ def test_paper_sample_run_1000x1000_50_seeds(vd):
         if f % 10 == 9:
             assert d.label_hash() == oracle.label_hash(G), f
     assert np.array_equal(d.labels(), G)
+
+
+# ---------------------------------------------------------------- windowed fast pass (REL)
+# For 32768 < N <= 65536 the fast kernel works in 16-bit coordinates relative to a
+# 32768-wide window around each walk; a walk that meets a label outside its window is
+# recomputed with 64-bit keys.  Both halves are checked against the oracle over the whole
+# grid: jittered maps (labels near their pixel, the converged-dJFA case) sprinkled with
+# far labels (forcing the exact recomputation), and fully random maps (every walk falls back).
+
+def _jittered_map(N, jitter, far, seed):
+    rng = np.random.default_rng(seed)
+    G = np.empty((N, N), dtype=np.uint32)
+    x = np.arange(N, dtype=np.int64)
+    for y0 in range(0, N, 2048):
+        y1 = min(N, y0 + 2048)
+        ys = np.arange(y0, y1, dtype=np.int64)[:, None]
+        lx = np.clip(x[None, :] + rng.integers(-jitter, jitter + 1, size=(y1 - y0, N)), 0, N - 1)
+        ly = np.clip(ys + rng.integers(-jitter, jitter + 1, size=(y1 - y0, N)), 0, N - 1)
+        G[y0:y1] = ((ly << 16) | lx).astype(np.uint32)
+    n = far
+    py, px = rng.integers(0, N, n), rng.integers(0, N, n)
+    G[py, px] = ((rng.integers(0, N, n) << 16) | rng.integers(0, N, n)).astype(np.uint32)
+    return G
+
+
+@pytest.fixture(scope="module")
+def rel_grid():
+    N = 36000  # > 32768 (windowed path), ragged against the 512-column CTA tile
+    return N, _jittered_map(N, 40, 3000, 77)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k,metric,vn", [(1, "euclid", False), (2, "euclid", False), (4, "euclid", False),
+                                         (64, "euclid", False), (4096, "euclid", False),
+                                         (8, "manhattan", False), (16, "euclid", True)])
+def test_windowed_pass_bit_exact(vd, rel_grid, k, metric, vn):
+    N, G = rel_grid
+    d = vd.VoronoiDiagram(N, np.array([0, 0], dtype=np.uint16), metric=metric)
+    d.set_labels(G)
+    d.jump_pass(k, von_neumann=vn)
+    got = d.labels()
+    d.close()
+    want = oracle.jump_pass(G, k, metric=metric, vn=vn)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, (k, bad[:5].tolist(), len(bad))
+
+
+@pytest.mark.slow
+def test_windowed_pass_all_far_labels(vd):
+    N, k = 33000, 8
+    rng = np.random.default_rng(5)
+    G = ((rng.integers(0, N, (N, N), dtype=np.uint32) << 16) | rng.integers(0, N, (N, N), dtype=np.uint32))
+    d = vd.VoronoiDiagram(N, np.array([0, 0], dtype=np.uint16))
+    d.set_labels(G)
+    d.jump_pass(k)
+    got = d.labels()
+    d.close()
+    assert np.array_equal(got, oracle.jump_pass(G, k))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [1, 16, 2048])
+def test_windowed_pass_with_empty_bit_exact(vd, rel_grid, k):
+    # MAY_EMPTY windowed path: EMPTY labels sprinkled in (walks meeting one are recomputed).
+    N, G0 = rel_grid
+    G = G0.copy()
+    rng = np.random.default_rng(k)
+    G[rng.integers(0, N, 5000), rng.integers(0, N, 5000)] = EMPTY
+    G[1000:1003] = EMPTY  # whole empty rows
+    d = vd.VoronoiDiagram(N, np.array([0, 0], dtype=np.uint16))
+    d.set_labels(G)
+    d.jump_pass(k)
+    got = d.labels()
+    d.close()
+    assert np.array_equal(got, oracle.jump_pass(G, k))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("N,s", [(20000, 25000), (33000, 4000)])
+def test_jfa_large_grid_bit_exact(vd, N, s):
+    # JFA beyond the plain fast kernel's range: the first passes (k > 4096) run the 64-bit
+    # kernel, the rest the windowed one with EMPTY present.
+    xy = synth.uniform_seeds(N, s, rng_seed=N)
+    d = _jfa_gpu(vd, N, xy)
+    got = d.labels()
+    d.close()
+    assert np.array_equal(got, oracle.jfa(N, xy))
