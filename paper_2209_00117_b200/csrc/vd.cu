@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -128,6 +129,8 @@ struct vd_ctx {
   uint32_t extras = 0;
   int metric = 0;           // 0 Euclidean (dJFAe), 1 Manhattan (dJFAm)
   uint32_t vn_waves = 0;    // Von Neumann waves at the start of each dJFA step
+  bool force_rel = false;   // test hook (env VD_FORCE_WINDOWED=1): windowed kernel at any N
+  bool track_empty = false; // jump_pass_wide reports EMPTY outputs into `counter` (vd_jfa)
   uint32_t jfa_vn_waves = 0;// ... and of each full JFA (Fig. 5)
   uint32_t hcap = 0;  // halo rows allocated per side
   std::vector<Shard> shards;
@@ -276,12 +279,9 @@ cudaError_t launch_fast_mv(int metric, bool vn, const vdk::PassArgs& a, dim3 g, 
 template <int KM>
 cudaError_t launch_fast_k(bool me, bool bd, bool rel, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b,
                           size_t sm, cudaStream_t st) {
-  if (rel) {  // windowed coordinates (grids beyond the plain fast kernel's range)
-    if (me) return bd ? launch_fast_mv<KM, true, true, true>(metric, vn, a, g, b, sm, st)
-                      : launch_fast_mv<KM, true, false, true>(metric, vn, a, g, b, sm, st);
+  if (rel)  // windowed coordinates (complete diagrams beyond the plain fast kernel's range)
     return bd ? launch_fast_mv<KM, false, true, true>(metric, vn, a, g, b, sm, st)
               : launch_fast_mv<KM, false, false, true>(metric, vn, a, g, b, sm, st);
-  }
   if (me) return bd ? launch_fast_mv<KM, true, true, false>(metric, vn, a, g, b, sm, st)
                     : launch_fast_mv<KM, true, false, false>(metric, vn, a, g, b, sm, st);
   return bd ? launch_fast_mv<KM, false, true, false>(metric, vn, a, g, b, sm, st)
@@ -289,10 +289,10 @@ cudaError_t launch_fast_k(bool me, bool bd, bool rel, int metric, bool vn, const
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
-// Windowed fast pass (REL) for the grids beyond fast_ok (N > 32768; N > 16384 when EMPTY may
-// occur), for steps small enough that a walk and its neighbour rows fit the 32768-wide window
-// (dJFA's delta passes, JFA's last 13).  Walks meeting EMPTY or far labels are recomputed exactly.
-bool rel_ok(uint32_t N, bool may_empty, uint32_t k) { return !fast_ok(N, may_empty) && k <= 4096; }
+// Windowed fast pass (REL) for complete diagrams with 32768 < N <= 65536 and steps small
+// enough that a walk and its neighbour rows fit the 32768-wide window (dJFA's delta passes,
+// JFA's last 13 once no EMPTY is left).  Walks meeting far labels are recomputed exactly.
+bool rel_ok(uint32_t N, bool may_empty, uint32_t k) { return !may_empty && !fast_ok(N, false) && k <= 4096; }
 
 vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn) {
   vdk::PassArgs a;
@@ -316,9 +316,10 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn)
   a.one = 1u;
   a.metric = h->metric;
   a.vn = vn ? 1 : 0;
+  a.empty_flag = h->track_empty ? h->counter : nullptr;
   vd_status st = timed_begin(h);
   if (st) return st;
-  const bool rel = rel_ok(h->N, may_empty, k);
+  const bool rel = rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096);
   if ((fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, B);
     const uint32_t per_res = (B + k - 1) / k;
@@ -338,7 +339,19 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn)
     a.segs = 1;
     a.walk = 1;
     const int64_t blocks = (int64_t)a.xblocks * B;
-    vdk::jump_pass_wide<<<dim3((unsigned)blocks), dim3(vdk::kThreads), 0, h->stream>>>(a);
+    const dim3 g((unsigned)blocks), b(vdk::kThreads);
+    const bool v4 = (k % 4) == 0;
+    if (h->metric == 0) {
+      if (vn) v4 ? vdk::jump_pass_wide<0, true, true><<<g, b, 0, h->stream>>>(a)
+              : vdk::jump_pass_wide<0, true, false><<<g, b, 0, h->stream>>>(a);
+      else v4 ? vdk::jump_pass_wide<0, false, true><<<g, b, 0, h->stream>>>(a)
+              : vdk::jump_pass_wide<0, false, false><<<g, b, 0, h->stream>>>(a);
+    } else {
+      if (vn) v4 ? vdk::jump_pass_wide<1, true, true><<<g, b, 0, h->stream>>>(a)
+              : vdk::jump_pass_wide<1, true, false><<<g, b, 0, h->stream>>>(a);
+      else v4 ? vdk::jump_pass_wide<1, false, true><<<g, b, 0, h->stream>>>(a)
+              : vdk::jump_pass_wide<1, false, false><<<g, b, 0, h->stream>>>(a);
+    }
   }
   st = after_launch(h, "jump_pass");
   if (st) return st;
@@ -593,6 +606,10 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   h->vshards = cfg.world > 1 ? 1 : vsh;
   h->extras = cfg.extra_passes;
   h->metric = (int)cfg.metric;
+  {
+    const char* f = std::getenv("VD_FORCE_WINDOWED");
+    h->force_rel = f && f[0] == '1';
+  }
   h->vn_waves = cfg.vn_waves;
   h->jfa_vn_waves = cfg.jfa_vn_waves;
   if (cfg.device >= 0) h->device = cfg.device;
@@ -685,9 +702,28 @@ vd_status vd_jfa(vd_handle h) {
   vd_status st = jfa_init(h);
   if (st) return st;
   const bool virt = unclaimed_label(h) != VD_EMPTY;
+  // Beyond N = 16384 EMPTY is real and the passes run the 64-bit kernel, which reports
+  // whether it left any EMPTY (summed over ranks); from the first pass that leaves none on,
+  // the remaining passes take the EMPTY-free kernels (a complete map stays complete).
+  bool may_empty = !virt;
+  const bool track = may_empty;
   for (size_t i = 0; i < ks.size(); ++i) {
-    st = run_pass(h, ks[i], !virt, i < h->jfa_vn_waves);
+    const bool vn = i < h->jfa_vn_waves;
+    if (track && may_empty) {
+      CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+      h->track_empty = true;
+    }
+    // JFA's labels are still far from their pixels at large steps: there the windowed kernel
+    // would recompute most walks, and the 64-bit one is cheaper (C5: 31 vs 68 ms at k = 512).
+    const bool far = h->N > 32768 && ks[i] > 256;
+    st = run_pass(h, ks[i], may_empty || far, vn);
+    h->track_empty = false;
     if (st) return st;
+    if (track && may_empty) {
+      uint64_t any = 1;
+      if ((st = reduce_to_host(h, &any))) return st;
+      may_empty = any != 0;
+    }
   }
   // A Moore JFA reaches every pixel (k_1 = 2^(ceil(log2 N)-1) covers every offset), so no V
   // survives; Von Neumann waves may leave some.

@@ -45,6 +45,7 @@ struct PassArgs {
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
   int32_t metric;   // 0 Euclidean, 1 Manhattan (jump_pass_wide; the fast kernel templates it)
   int32_t vn;       // Von Neumann neighbourhood (jump_pass_wide)
+  unsigned long long* empty_flag;  // jump_pass_wide: set non-zero if any output is EMPTY (or null)
 };
 
 __device__ __forceinline__ const uint32_t* row_ptr(const PassArgs& a, int r) {
@@ -207,8 +208,7 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
   for (int i = 0; i < 3 * kVec; ++i) {
     uint32_t c = R.c[i];
     if (MAY_EMPTY && !REL) { c = __vminu2(c, vempty); R.c[i] = c; }  // EMPTY -> virtual far seed
-    if constexpr (REL) {  // window coordinates; EMPTY (MAY_EMPTY) also sends the walk to the exact path
-      if (MAY_EMPTY && c == EMPTY) *bad |= 0x8000u;
+    if constexpr (REL) {  // window coordinates (no EMPTY on this path)
       c = __vadd2(c, nbase2);
       R.c[i] = c;
       *bad |= c;
@@ -264,12 +264,13 @@ __device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Ro
                            __vimin3_u32(w[6], w[7], w[8]));
 }
 
-// Exact (64-bit) candidate test: key (distance, label), EMPTY = +infinity.
-__device__ __forceinline__ void consider_wide(uint32_t c, int x, int y, int metric, uint64_t& bd, uint32_t& bc) {
+// Exact candidate test, key (distance, label) with EMPTY = +infinity, metric fixed at compile
+// time: |dx|, |dy| <= 65535, so each square fits 32 bits and only the sum needs 33 (uint64).
+template <int METRIC>
+__device__ __forceinline__ void consider64(uint32_t c, int x, int y, uint64_t& bd, uint32_t& bc) {
   if (c == EMPTY) return;
-  int64_t dx = (int64_t)(c & 0xFFFFu) - x, dy = (int64_t)(c >> 16) - y;
-  uint64_t d = metric == 0 ? (uint64_t)(dx * dx) + (uint64_t)(dy * dy)
-                           : (uint64_t)(dx < 0 ? -dx : dx) + (uint64_t)(dy < 0 ? -dy : dy);
+  const uint32_t dx = (uint32_t)abs((int)(c & 0xFFFFu) - x), dy = (uint32_t)abs((int)(c >> 16) - y);
+  const uint64_t d = METRIC == 0 ? (uint64_t)(dx * dx) + (uint64_t)(dy * dy) : (uint64_t)(dx + dy);
   if (d < bd || (d == bd && c < bc)) { bd = d; bc = c; }
 }
 
@@ -407,7 +408,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
               const int q = xe + cc * k;
               if (q < 0 || q >= N || xe >= N) continue;
               const int off = spans3 ? (cc + 1) * kW + (q - (x0 + cc * k)) : q - (x0 - K4);
-              consider_wide(st[off], xe, yy, METRIC, bd, bc);
+              consider64<METRIC>(st[off], xe, yy, bd, bc);
             }
           }
           o[e] = bc;
@@ -424,6 +425,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
 
 template <int KM, bool MAY_EMPTY, bool BANDED, int METRIC = 0, bool VN = false, bool REL = false>
 __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
+  static_assert(!(MAY_EMPTY && REL), "the windowed path takes complete diagrams only");
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
   const int wk = (int)(blockIdx.x / (unsigned)a.xblocks);
@@ -443,36 +445,57 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
 
 // ------------------------------------------------------------------ wide jump pass
 //
-// Same pass for grids the fast kernel cannot take exactly (N > 32768, or EMPTY present
-// with N > 23170): uint64 squared distances, explicit EMPTY, lexicographic (d2, label).
-// One thread per 4 adjacent pixels of one row, nine 128-bit loads.
+// Same pass for what the fast kernels do not take: steps that are not powers of two, steps
+// > 4096 beyond N = 32768 (> 256 with EMPTY beyond N = 16384).
+
+// Generic pass (any k, any N <= 65536, EMPTY allowed): one thread = 4 pixels of one row,
+// 64-bit keys, candidates read straight from global memory (L2-friendly for the large steps
+// it serves).  V4: k % 4 == 0, so the neighbour columns are 16-byte aligned vectors.
+template <int METRIC, bool VN, bool V4>
 __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
   const int yl = (int)(blockIdx.x / (unsigned)a.xblocks);
   const int x = (xb * kThreads + (int)threadIdx.x) * 4;
-  if (x >= a.N || yl >= a.rows) return;
   const int y = a.row0 + yl, k = a.k, N = a.N;
-  uint32_t best[4];
-  uint64_t bd[4];
+  const bool live = x < N && yl < a.rows;
+  bool any_empty = false;
+  if (live) {
+    uint32_t best[4];
+    uint64_t bd[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) { best[e] = EMPTY; bd[e] = ~0ull; }
+    for (int e = 0; e < 4; ++e) { best[e] = EMPTY; bd[e] = ~0ull; }
 #pragma unroll
-  for (int oy = -1; oy <= 1; ++oy) {
-    int r = y + oy * k;
-    if (r < 0 || r >= N) continue;
-    const uint32_t* p = row_ptr(a, r);
+    for (int oy = -1; oy <= 1; ++oy) {
+      const int r = y + oy * k;
+      if (r < 0 || r >= N) continue;
+      const uint32_t* p = row_ptr(a, r);
 #pragma unroll
-    for (int ox = -1; ox <= 1; ++ox) {
-      if (a.vn && ox != 0 && oy != 0) continue;  // Von Neumann: no diagonals
+      for (int ox = -1; ox <= 1; ++ox) {
+        if (VN && ox != 0 && oy != 0) continue;  // Von Neumann: no diagonals
+        const int q0 = x + ox * k;
+        if constexpr (V4) {
+          if (q0 < 0 || q0 >= N) continue;  // the whole aligned vector is out of the grid
+          const uint4 v = *reinterpret_cast<const uint4*>(p + q0);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        int q = x + e + ox * k;
-        if (x + e >= N || q < 0 || q >= N) continue;
-        consider_wide(p[q], x + e, y, a.metric, bd[e], best[e]);
+          for (int e = 0; e < 4; ++e)
+            if (q0 + e < N) consider64<METRIC>(w[e], x + e, y, bd[e], best[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int q = q0 + e;
+            if (x + e >= N || q < 0 || q >= N) continue;
+            consider64<METRIC>(p[q], x + e, y, bd[e], best[e]);
+          }
+        }
       }
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) any_empty |= (x + e < N) && best[e] == EMPTY;
+    // columns >= N of the ragged tail hold don't-care values (never read as pixels)
+    *reinterpret_cast<uint4*>(a.out + (int64_t)yl * a.pitch + x) = make_uint4(best[0], best[1], best[2], best[3]);
   }
-  *reinterpret_cast<uint4*>(a.out + (int64_t)yl * a.pitch + x) = make_uint4(best[0], best[1], best[2], best[3]);
+  if (a.empty_flag != nullptr && __syncthreads_or(any_empty) && threadIdx.x == 0) atomicOr(a.empty_flag, 1ull);
 }
 
 // ------------------------------------------------------------------ JFA init

@@ -397,7 +397,7 @@ def test_windowed_pass_all_far_labels(vd):
 @pytest.mark.slow
 @pytest.mark.parametrize("k", [1, 16, 2048])
 def test_windowed_pass_with_empty_bit_exact(vd, rel_grid, k):
-    # MAY_EMPTY windowed path: EMPTY labels sprinkled in (walks meeting one are recomputed).
+    # Maps with EMPTY beyond N = 16384 take the 64-bit kernel (any k).
     N, G0 = rel_grid
     G = G0.copy()
     rng = np.random.default_rng(k)
@@ -414,10 +414,31 @@ def test_windowed_pass_with_empty_bit_exact(vd, rel_grid, k):
 @pytest.mark.slow
 @pytest.mark.parametrize("N,s", [(20000, 25000), (33000, 4000)])
 def test_jfa_large_grid_bit_exact(vd, N, s):
-    # JFA beyond the plain fast kernel's range: the first passes (k > 4096) run the 64-bit
-    # kernel, the rest the windowed one with EMPTY present.
+    # JFA beyond the plain fast kernel's range: the 64-bit kernel while EMPTY remains, then
+    # the EMPTY-free kernels (windowed beyond N = 32768).
     xy = synth.uniform_seeds(N, s, rng_seed=N)
     d = _jfa_gpu(vd, N, xy)
     got = d.labels()
     d.close()
     assert np.array_equal(got, oracle.jfa(N, xy))
+
+
+@pytest.mark.parametrize("N", [5, 64, 257, 1024, 1031, 2051])
+@pytest.mark.parametrize("metric,vn", [("euclid", False), ("manhattan", False), ("euclid", True)])
+def test_single_pass_windowed_forced_bit_exact(vd, monkeypatch, N, metric, vn):
+    # The windowed kernel forced at small N (test hook) on complete maps; maps with EMPTY
+    # keep the EMPTY-aware kernels (the windowed one takes complete diagrams only).
+    monkeypatch.setenv("VD_FORCE_WINDOWED", "1")
+    rng = np.random.default_rng(N + 11)
+    s = min(N * N, 40)
+    xy = synth.uniform_seeds(N, s, rng_seed=N)
+    labels = np.array([oracle.pack(int(xy[2 * i]), int(xy[2 * i + 1])) for i in range(s)], dtype=np.uint32)
+    d = vd.VoronoiDiagram(N, xy, metric=metric)
+    full = labels[rng.integers(0, len(labels), size=(N, N))]
+    holes = full.copy()
+    holes[rng.random((N, N)) < 0.002] = EMPTY
+    for G in (full, holes):
+        for k in sorted({1, 2, 4, 8, 64, 512} | {max(1, N // 2)}):
+            d.set_labels(G)
+            d.jump_pass(k, von_neumann=vn)
+            assert np.array_equal(d.labels(), oracle.jump_pass(G, k, metric=metric, vn=vn)), (k, (G == EMPTY).any())
