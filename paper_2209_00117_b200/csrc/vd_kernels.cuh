@@ -213,11 +213,13 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
       R.c[i] = c;
       *bad |= c;
     }
-    const int cy = (int)(c >> 16);
-    R.cy[i] = cy;
+    // uint32 arithmetic throughout (wrapping is defined; labels outside a window give
+    // don't-care values there, never undefined behaviour)
+    const uint32_t cy = c >> 16;
+    R.cy[i] = (int)cy;
     if constexpr (METRIC == 0) {
-      const int D = (int)(c * sh16) + xs16[i % kVec];         // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
-      R.q[i] = cy * cy + __mulhi(D, D);                        // cy^2 + dx^2
+      const uint32_t D = c * sh16 + (uint32_t)xs16[i % kVec];  // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
+      R.q[i] = (int)(cy * cy + (uint32_t)__mulhi((int)D, (int)D));  // cy^2 + dx^2
     } else {
       R.q[i] = (int)__sad((int)(c & 0xFFFFu), (REL ? xr : x) + (i % kVec), 0u);  // |cx - (x+e)|
     }
@@ -237,7 +239,7 @@ __device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Ro
   uint32_t c[9];
   int d[9];
   auto dist = [&](const Row& R, int i) -> int {
-    if constexpr (METRIC == 0) return R.q[i] + R.cy[i] * (-2 * y);
+    if constexpr (METRIC == 0) return (int)((uint32_t)R.q[i] + (uint32_t)R.cy[i] * (uint32_t)(-2 * y));
     else return (int)__sad(R.cy[i], y, (unsigned)R.q[i]);
   };
   if constexpr (!VN) {
