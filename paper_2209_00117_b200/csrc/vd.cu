@@ -142,6 +142,8 @@ struct vd_ctx {
   int disp_slot = 0;
   cudaEvent_t disp_used[2] = {nullptr, nullptr};  // last kernel reading each slot done
   cudaStream_t copy_stream = nullptr;             // host -> device uploads
+  cudaStream_t halo_stream = nullptr;             // halo exchange overlapped with interior rows
+  cudaEvent_t halo_ready = nullptr, halo_done = nullptr;
   cudaEvent_t copy_done = nullptr;
   uint32_t* fwd = nullptr;        // [N*N] forward map (dJFA), allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
@@ -294,7 +296,9 @@ bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 
 // JFA's last 13 once no EMPTY is left).  Walks meeting far labels are recomputed exactly.
 bool rel_ok(uint32_t N, bool may_empty, uint32_t k) { return !may_empty && !fast_ok(N, false) && k <= 4096; }
 
-vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn) {
+// One pass over output rows [y_lo, y_hi) of shard sh (global rows; default: the whole band).
+vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn, int64_t y_lo = -1,
+                      int64_t y_hi = -1) {
   vdk::PassArgs a;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
@@ -317,12 +321,15 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn)
   a.metric = h->metric;
   a.vn = vn ? 1 : 0;
   a.empty_flag = h->track_empty ? h->counter : nullptr;
-  vd_status st = timed_begin(h);
-  if (st) return st;
+  if (y_lo < 0) { y_lo = (int64_t)sh.row0; y_hi = (int64_t)(sh.row0 + sh.rows); }
+  a.y_lo = (int)y_lo;
+  a.y_hi = (int)y_hi;
+  const uint32_t R = (uint32_t)(y_hi - y_lo);  // output rows of this launch
+  if (R == 0) return VD_OK;
   const bool rel = rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096);
   if ((fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
-    const uint32_t nres = std::min(k, B);
-    const uint32_t per_res = (B + k - 1) / k;
+    const uint32_t nres = std::min(k, R);
+    const uint32_t per_res = (R + k - 1) / k;
     a.walk = vdk::walk_len((int)k);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
@@ -338,7 +345,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn)
   } else {
     a.segs = 1;
     a.walk = 1;
-    const int64_t blocks = (int64_t)a.xblocks * B;
+    const int64_t blocks = (int64_t)a.xblocks * R;
     const dim3 g((unsigned)blocks), b(vdk::kThreads);
     const bool v4 = (k % 4) == 0;
     if (h->metric == 0) {
@@ -353,13 +360,12 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn)
               : vdk::jump_pass_wide<1, false, false><<<g, b, 0, h->stream>>>(a);
     }
   }
-  st = after_launch(h, "jump_pass");
-  if (st) return st;
-  return timed_end(h, (uint64_t)B * h->N);
+  return after_launch(h, "jump_pass");
 }
 
 // Halo exchange for step k (vd_halo_plan), then one pass on every local shard.
-vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
+// Halo exchange of one pass (vd_halo_plan) on stream `st`.
+vd_status exchange_halos(vd_ctx* h, uint32_t k, cudaStream_t st) {
   const size_t row_bytes = (size_t)h->pitch * sizeof(uint32_t);
   if (h->world > 1) {
     vd_halo_plan_t p;
@@ -368,12 +374,12 @@ vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
     const size_t cnt = (size_t)p.halo_rows * h->pitch;
     CKN(g_nccl.GroupStart());
     if (p.recv_top_rank >= 0) {
-      CKN(g_nccl.Recv(sh.top, cnt, ncclUint32, p.recv_top_rank, h->comm, h->stream));
-      CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_top_row0 * h->pitch, cnt, ncclUint32, p.recv_top_rank, h->comm, h->stream));
+      CKN(g_nccl.Recv(sh.top, cnt, ncclUint32, p.recv_top_rank, h->comm, st));
+      CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_top_row0 * h->pitch, cnt, ncclUint32, p.recv_top_rank, h->comm, st));
     }
     if (p.recv_bot_rank >= 0) {
-      CKN(g_nccl.Recv(sh.bot, cnt, ncclUint32, p.recv_bot_rank, h->comm, h->stream));
-      CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_bot_row0 * h->pitch, cnt, ncclUint32, p.recv_bot_rank, h->comm, h->stream));
+      CKN(g_nccl.Recv(sh.bot, cnt, ncclUint32, p.recv_bot_rank, h->comm, st));
+      CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_bot_row0 * h->pitch, cnt, ncclUint32, p.recv_bot_rank, h->comm, st));
     }
     CKN(g_nccl.GroupEnd());
   } else if (h->vshards > 1) {
@@ -383,16 +389,51 @@ vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
       Shard& sh = h->shards[g];
       if (p.recv_top_rank >= 0)
         CK(cudaMemcpyAsync(sh.top, h->shards[p.recv_top_rank].buf[h->cur] + (size_t)(sh.rows - p.halo_rows) * h->pitch,
-                           p.halo_rows * row_bytes, cudaMemcpyDeviceToDevice, h->stream));
+                           p.halo_rows * row_bytes, cudaMemcpyDeviceToDevice, st));
       if (p.recv_bot_rank >= 0)
         CK(cudaMemcpyAsync(sh.bot, h->shards[p.recv_bot_rank].buf[h->cur], p.halo_rows * row_bytes,
-                           cudaMemcpyDeviceToDevice, h->stream));
+                           cudaMemcpyDeviceToDevice, st));
     }
   }
-  for (auto& sh : h->shards) {
-    vd_status st = launch_pass(h, sh, k, may_empty, vn);
-    if (st) return st;
+  return VD_OK;
+}
+
+// One pass on every shard.  Sharded with k < B/2: the halos travel on halo_stream while the
+// interior rows [k, B-k) of each band, which read no halo, are computed; then the two edge
+// strips ("compute interior rows while the halos are in flight").
+vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
+  vd_status st;
+  const bool sharded = h->world > 1 || h->vshards > 1;
+  const bool overlap = sharded && 2 * k < h->shards[0].rows;
+  if (!overlap) {
+    if (sharded && (st = exchange_halos(h, k, h->stream))) return st;
+    for (auto& sh : h->shards) {
+      if ((st = timed_begin(h))) return st;
+      if ((st = launch_pass(h, sh, k, may_empty, vn))) return st;
+      if ((st = timed_end(h, (uint64_t)sh.rows * h->N))) return st;
+    }
+    h->cur ^= 1;
+    return VD_OK;
   }
+  CK(cudaEventRecord(h->halo_ready, h->stream));  // this pass's input is complete
+  CK(cudaStreamWaitEvent(h->halo_stream, h->halo_ready, 0));
+  if ((st = exchange_halos(h, k, h->halo_stream))) return st;
+  CK(cudaEventRecord(h->halo_done, h->halo_stream));
+  // one timed interval per pass: first interior launch .. last edge strip
+  if ((st = timed_begin(h))) return st;
+  uint64_t px = 0;
+  for (auto& sh : h->shards) {  // interior rows read no halo
+    const int64_t r0 = (int64_t)sh.row0, r1 = r0 + (int64_t)sh.rows;
+    if ((st = launch_pass(h, sh, k, may_empty, vn, r0 + k, r1 - k))) return st;
+    px += (uint64_t)sh.rows * h->N;
+  }
+  CK(cudaStreamWaitEvent(h->stream, h->halo_done, 0));
+  for (auto& sh : h->shards) {
+    const int64_t r0 = (int64_t)sh.row0, r1 = r0 + (int64_t)sh.rows;
+    if ((st = launch_pass(h, sh, k, may_empty, vn, r0, r0 + k))) return st;  // top strip
+    if ((st = launch_pass(h, sh, k, may_empty, vn, r1 - k, r1))) return st;  // bottom strip
+  }
+  if ((st = timed_end(h, px))) return st;
   h->cur ^= 1;
   return VD_OK;
 }
@@ -461,6 +502,9 @@ void free_all(vd_ctx* h) {
     if (e) cudaEventDestroy(e);
   if (h->copy_done) cudaEventDestroy(h->copy_done);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->halo_stream) cudaStreamDestroy(h->halo_stream);
+  if (h->halo_ready) cudaEventDestroy(h->halo_ready);
+  if (h->halo_done) cudaEventDestroy(h->halo_done);
   for (auto e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
   if (h->comm && g_nccl.ok) g_nccl.CommDestroy(h->comm);
@@ -666,6 +710,9 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   CKC(cudaMalloc(&h->disp_buf[0], s * sizeof(short2)));
   CKC(cudaMalloc(&h->disp_buf[1], s * sizeof(short2)));
   CKC(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&h->halo_stream, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&h->halo_ready, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&h->halo_done, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&h->copy_done, cudaEventDisableTiming));
   for (auto& e : h->disp_used) {
     CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -37,6 +37,8 @@ struct PassArgs {
   uint32_t* __restrict__ out;
   int64_t pitch;
   int32_t N, row0, rows, top_row0, bot_row0, k;
+  int32_t y_lo, y_hi;  // output rows [y_lo, y_hi) (global), inside the band: the whole band, or the
+                       // interior / an edge strip when the halo exchange is overlapped
   int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / walk)
   int32_t walk;     // output rows per walk (walk_len(k))
   int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
@@ -290,7 +292,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   const int k = a.k, N = a.N;
   const int tid = (int)threadIdx.x;
   const int x = x0 + kVec * tid;
-  const int yend = a.row0 + a.rows;
+  const int yend = a.y_hi;
   const int nout = min(a.walk, (yend - y0 + k - 1) / k);  // output rows of this walk
   const int nlist = nout + 2;                              // staged input rows
   const bool spans3 = k >= kW;
@@ -433,8 +435,8 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassAr
   const int wk = (int)(blockIdx.x / (unsigned)a.xblocks);
   const int res = wk / a.segs, seg = wk - res * a.segs;
   const int x0 = xb * kW;
-  const int y0 = a.row0 + res + seg * a.walk * a.k;
-  if (res >= a.k || y0 >= a.row0 + a.rows) return;  // uniform over the CTA
+  const int y0 = a.y_lo + res + seg * a.walk * a.k;
+  if (res >= a.k || y0 >= a.y_hi) return;  // uniform over the CTA
   // CTAs whose vectors can be partly outside the grid (a vector that straddles N, or
   // k < kVec at the left edge) take the per-element path; for k >= kVec and N % kVec == 0
   // a neighbour vector is either wholly inside or wholly outside the grid, and the latter
@@ -458,8 +460,8 @@ __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
   const int yl = (int)(blockIdx.x / (unsigned)a.xblocks);
   const int x = (xb * kThreads + (int)threadIdx.x) * 4;
-  const int y = a.row0 + yl, k = a.k, N = a.N;
-  const bool live = x < N && yl < a.rows;
+  const int y = a.y_lo + yl, k = a.k, N = a.N;
+  const bool live = x < N && y < a.y_hi;
   bool any_empty = false;
   if (live) {
     uint32_t best[4];
@@ -495,7 +497,8 @@ __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) any_empty |= (x + e < N) && best[e] == EMPTY;
     // columns >= N of the ragged tail hold don't-care values (never read as pixels)
-    *reinterpret_cast<uint4*>(a.out + (int64_t)yl * a.pitch + x) = make_uint4(best[0], best[1], best[2], best[3]);
+    *reinterpret_cast<uint4*>(a.out + (int64_t)(y - a.row0) * a.pitch + x) =
+        make_uint4(best[0], best[1], best[2], best[3]);
   }
   if (a.empty_flag != nullptr && __syncthreads_or(any_empty) && threadIdx.x == 0) atomicOr(a.empty_flag, 1ull);
 }

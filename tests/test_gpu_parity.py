@@ -442,3 +442,24 @@ def test_single_pass_windowed_forced_bit_exact(vd, monkeypatch, N, metric, vn):
             d.set_labels(G)
             d.jump_pass(k, von_neumann=vn)
             assert np.array_equal(d.labels(), oracle.jump_pass(G, k, metric=metric, vn=vn)), (k, (G == EMPTY).any())
+
+
+@pytest.mark.parametrize("G,metric,vn", [(4, "euclid", False), (8, "manhattan", False), (2, "euclid", True)])
+def test_virtual_shards_single_pass_bit_exact(vd, G, metric, vn):
+    # Sharded passes with the halo exchange overlapped (interior rows, then the two edge
+    # strips once the halos landed; 2k < band) and not (2k >= band), on arbitrary maps with
+    # EMPTY: fast kernel for powers of two, the 64-bit one otherwise.
+    N = 2048
+    rng = np.random.default_rng(G)
+    s = 60
+    xy = synth.uniform_seeds(N, s, rng_seed=G)
+    labels = np.array([oracle.pack(int(xy[2 * i]), int(xy[2 * i + 1])) for i in range(s)] + [EMPTY], dtype=np.uint32)
+    G_map = labels[rng.integers(0, len(labels), size=(N, N))]
+    d = vd.VoronoiDiagram(N, xy, metric=metric, virtual_shards=G)
+    B = N // G
+    for k in sorted({1, 2, 3, 4, 8, 64, B // 2 - 1, B // 2, B - 1, B, 2 * B} & set(range(1, N))):
+        if k > B and k % B:
+            continue
+        d.set_labels(G_map)
+        d.jump_pass(k, von_neumann=vn)
+        assert np.array_equal(d.labels(), oracle.jump_pass(G_map, k, metric=metric, vn=vn)), k
