@@ -267,7 +267,8 @@ cudaError_t launch_fast(const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, 
   static cudaError_t attr = cudaErrorNotReady;
   if (attr == cudaErrorNotReady)
     attr = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, vdk::kSmemBudget);
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                REL ? vdk::kSmemBudgetRel : vdk::kSmemBudget);
   if (attr != cudaSuccess) return attr;
   vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL><<<grid, blk, sm, st>>>(a);
   return cudaSuccess;
@@ -330,13 +331,13 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   if ((fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, R);
     const uint32_t per_res = (R + k - 1) / k;
-    a.walk = vdk::walk_len((int)k);
+    a.walk = vdk::walk_len((int)k, rel);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
     const bool banded = sh.top != nullptr;
-    const size_t sm = vdk::pass_smem((int)k);
+    const size_t sm = vdk::pass_smem((int)k, rel);
     cudaError_t e;
     if (k == 1) e = launch_fast_k<1>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     else if (k == 2) e = launch_fast_k<2>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);

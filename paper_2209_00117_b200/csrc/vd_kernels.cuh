@@ -123,8 +123,18 @@ constexpr int kW = kVec * kThreads;      // columns per CTA (512)
 #ifndef VD_SMEM_KB
 #define VD_SMEM_KB 56
 #endif
+#ifndef VD_REL_MAX_WALK
+#define VD_REL_MAX_WALK 32
+#endif
+#ifndef VD_REL_SMEM_KB
+#define VD_REL_SMEM_KB 72
+#endif
 constexpr int kMaxWalk = VD_MAX_WALK;    // output rows per walk (upper bound)
 constexpr int kSmemBudget = VD_SMEM_KB * 1024;  // staged rows per CTA
+// The windowed variant (REL) runs 3 CTAs per SM (its extra live values spill at 4), so each
+// CTA can stage more rows: longer walks amortise the two extra staged rows per walk.
+constexpr int kMaxWalkRel = VD_REL_MAX_WALK;
+constexpr int kSmemBudgetRel = VD_REL_SMEM_KB * 1024;
 
 // Elements of one staged input row: columns [x0 - K4, x0 + W + K4) when k < W (K4 = k
 // rounded up to 4), else three W-wide spans at x0 - k, x0, x0 + k.
@@ -132,12 +142,13 @@ __host__ __device__ inline int stage_elems(int k) {
   return k >= kW ? 3 * kW : kW + 2 * ((k + 3) & ~3);
 }
 // Output rows per walk so that walk + 2 staged rows fit the budget.
-__host__ __device__ inline int walk_len(int k) {
-  const int rows = kSmemBudget / (stage_elems(k) * 4 + 8);
-  return rows - 2 < 1 ? 1 : (rows - 2 > kMaxWalk ? kMaxWalk : rows - 2);
+__host__ __device__ inline int walk_len(int k, bool rel = false) {
+  const int rows = (rel ? kSmemBudgetRel : kSmemBudget) / (stage_elems(k) * 4 + 8);
+  const int mx = rel ? kMaxWalkRel : kMaxWalk;
+  return rows - 2 < 1 ? 1 : (rows - 2 > mx ? mx : rows - 2);
 }
-__host__ __device__ inline size_t pass_smem(int k) {
-  return (size_t)(walk_len(k) + 2) * (stage_elems(k) * 4 + 8);
+__host__ __device__ inline size_t pass_smem(int k, bool rel = false) {
+  return (size_t)(walk_len(k, rel) + 2) * (stage_elems(k) * 4 + 8);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -427,8 +438,11 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   }
 }
 
+#ifndef VD_REL_MIN_BLOCKS
+#define VD_REL_MIN_BLOCKS 3
+#endif
 template <int KM, bool MAY_EMPTY, bool BANDED, int METRIC = 0, bool VN = false, bool REL = false>
-__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
   static_assert(!(MAY_EMPTY && REL), "the windowed path takes complete diagrams only");
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);

@@ -463,3 +463,22 @@ def test_virtual_shards_single_pass_bit_exact(vd, G, metric, vn):
         d.set_labels(G_map)
         d.jump_pass(k, von_neumann=vn)
         assert np.array_equal(d.labels(), oracle.jump_pass(G_map, k, metric=metric, vn=vn)), k
+
+
+@pytest.mark.slow
+def test_windowed_pass_full_c5_size_bit_exact(vd):
+    # BASELINE configs[4] size (65536^2, the reserved pixel included) in the launch
+    # configuration bench.py times: one windowed pass per dJFA step regime (k = 32, 4, 1) on a
+    # jittered complete map, the whole grid against the oracle.
+    N = 65536
+    G = _jittered_map(N, 24, 20000, 2209)
+    G[G == EMPTY] = oracle.pack(N - 2, N - 1)  # label (65535, 65535) is EMPTY itself (R-4)
+    d = vd.VoronoiDiagram(N, np.array([0, 0], dtype=np.uint16))
+    for k in (32, 4, 1):
+        d.set_labels(G)
+        d.jump_pass(k)
+        got = d.labels()
+        want = oracle.jump_pass(G, k)
+        assert np.array_equal(got, want), k
+        del got, want
+    d.close()
