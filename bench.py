@@ -215,7 +215,21 @@ def run_gpu(args):
                 idt.copy_(torch.frombuffer(bytearray(vd.vd_nccl_unique_id()), dtype=torch.uint8))
             dist.broadcast(idt, 0)
             nccl_id = bytes(idt.cpu().numpy().tobytes())
-        return dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
+        return dict(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id,
+                    peer_halos=world > 1 and args.halo == "peer")
+
+    halo_mode = ["nccl" if world > 1 else None]
+
+    def make(**extra):
+        h = vd.VoronoiDiagram(N, xy0, **handle_cfg(), **extra)
+        if world > 1 and args.halo == "peer":
+            # fused peer-memory halo push (NEXT-3); NCCL stays for steps with 2k >= band rows
+            try:
+                h.attach_peers()
+                halo_mode[0] = "peer (fused push, NVLink P2P) + nccl for 2k >= band"
+            except Exception as e:  # noqa: BLE001 -- fall back to the NCCL exchange, say so
+                print(f"peer halos unavailable ({e}); using NCCL", file=sys.stderr)
+        return h
 
     xy0 = synth.uniform_seeds(N, s, rng_seed=RNG)
     W, K = args.warmup, args.steps
@@ -229,8 +243,8 @@ def run_gpu(args):
         return torch.cuda.Event(enable_timing=True)
 
     # ---------------- dJFA: bootstrap (untimed), warmup, timed region
-    dj = vd.VoronoiDiagram(N, xy0, **handle_cfg())
-    jf = vd.VoronoiDiagram(N, xy0, **handle_cfg())
+    dj = make()
+    jf = make()
     dj.jfa()
     for f in range(W):
         dj.djfa_step(disp_dev[f], d)
@@ -279,7 +293,7 @@ def run_gpu(args):
     # ---------------- dJFAm (Manhattan) on the same frames: speed + similarity
     djm = None
     if not args.no_variants:
-        dm = vd.VoronoiDiagram(N, xy0, metric="manhattan", **handle_cfg())
+        dm = make(metric="manhattan")
         dm.jfa()
         for f in range(W):
             dm.djfa_step(disp_dev[f], d)
@@ -351,7 +365,7 @@ def run_gpu(args):
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"{args.config}: {cdesc}, dJFA time steps", "N": N, "seeds": s, "d_max": d,
-                       "passes_per_frame": passes, "parallelism": f"rowband{world}",
+                       "passes_per_frame": passes, "parallelism": f"rowband{world}", "halo": halo_mode[0],
                        "l2": f"inputs larger than L2 (two {4 * N * N / 2**30:g}-GiB ping-pong label buffers vs 126 MB L2)"},
             "gpix_pass_per_s": gpps,
             "jfa": {"value": jfps, "unit": "frames/s", "ms_per_frame": jms / K, "passes_per_frame": jpasses,
@@ -389,6 +403,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact-sample", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the dJFAm (Manhattan) measurement")
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: halo rows pushed by the pass kernels over peer memory, or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -84,7 +84,11 @@ typedef struct {
                                rest Moore ("Von Neumann for the first two
                                waves"); default 0 = Moore only                              */
     uint32_t jfa_vn_waves;  /* same for vd_jfa (Fig. 5 / P:163-168: Von Neumann-only JFA)   */
-    uint32_t reserved[3];   /* must be zero                                                */
+    uint32_t peer_halos;    /* 1: halo rows for the next pass are pushed by the pass kernels
+                               straight into the neighbouring bands' halo buffers (NEXT-3).
+                               virtual_shards: immediate; world > 1: after vd_peer_attach, and
+                               then nccl_id may be NULL (only steps with 2k < band rows run) */
+    uint32_t reserved[2];   /* must be zero                                                */
 } vd_config;
 
 /* Fill *cfg with defaults: device -1, stream NULL, rank 0, world 1, no extras,
@@ -138,6 +142,20 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max);
  * (vd_djfa_step is allowed) iff no label is EMPTY; the caller then guarantees every label
  * is a current seed position, as after vd_jfa.  Synchronises. */
 vd_status vd_set_labels(vd_handle h, const uint32_t* labels);
+
+/* Peer halos across processes (NEXT-3; SURVEY section 8(e) "device-initiated halo exchange").
+ * Each rank exports CUDA IPC handles of its halo buffers and flag words (vd_peer_export: writes
+ * *len = blob size bytes to out when cap suffices; out = NULL only queries *len), the caller
+ * all-gathers the blobs in rank order (e.g. torch.distributed.all_gather_object) and every rank
+ * calls vd_peer_attach(h, blobs, len) once before its next pass.  From then on a pass with
+ * 2k < B rows stores the rows its neighbours' next pass needs straight into their halo buffers
+ * from inside the pass kernel, and publishes a per-pass sequence number into their flag words
+ * (st.release.sys); the next pass's edge strips start after a device-side acquire wait.  The
+ * first pass of each call copies its edge rows the same way (push_rows).  A wait that does not
+ * complete within ~20 s sets a sticky flag readable with vd_peer_status (no hang). */
+vd_status vd_peer_export(vd_handle h, void* out, size_t cap, size_t* len);
+vd_status vd_peer_attach(vd_handle h, const void* blobs, size_t len_each);
+vd_status vd_peer_status(vd_handle h, uint32_t* timed_out);
 
 /* One jump pass with step k >= 1 on the current diagram (the body of every JFA / dJFA
  * wave, in gather form R-12), including the halo exchange when sharded, with

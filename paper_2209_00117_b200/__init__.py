@@ -24,7 +24,8 @@ __all__ = [
     "vd_djfa_step", "vd_stf", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
     "vd_get_seeds", "vd_band", "vd_last_passes", "vd_synchronize", "vd_set_pass_timing",
     "vd_pass_timing", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
-    "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "EXPORTED_SYMBOLS",
+    "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "vd_peer_export",
+    "vd_peer_attach", "vd_peer_status", "EXPORTED_SYMBOLS",
 ]
 
 EMPTY = 0xFFFFFFFF
@@ -55,7 +56,8 @@ class vd_config(ctypes.Structure):
         ("metric", ctypes.c_uint32),
         ("vn_waves", ctypes.c_uint32),
         ("jfa_vn_waves", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32 * 3),
+        ("peer_halos", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32 * 2),
     ]
 
 
@@ -101,6 +103,9 @@ _SIGS = {
                                       ctypes.POINTER(vd_halo_plan_t)]),
     "vd_set_labels": (ctypes.c_int32, [H, P]),
     "vd_pass": (ctypes.c_int32, [H, ctypes.c_uint32, ctypes.c_uint32]),
+    "vd_peer_export": (ctypes.c_int32, [H, P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "vd_peer_attach": (ctypes.c_int32, [H, P, ctypes.c_size_t]),
+    "vd_peer_status": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32)]),
     "vd_destroy": (None, [H]),
     "vd_status_str": (ctypes.c_char_p, [ctypes.c_int32]),
     "vd_last_error": (ctypes.c_char_p, [H]),
@@ -168,7 +173,7 @@ VD_PASS_VON_NEUMANN = 1
 
 def vd_create(N: int, seeds_xy, *, device: int = -1, stream: int | None = None, rank: int = 0, world: int = 1,
               nccl_id: bytes | None = None, extra_passes: int = 0, virtual_shards: int = 0, metric: str = "euclid",
-              vn_waves: int = 0, jfa_vn_waves: int = 0):
+              vn_waves: int = 0, jfa_vn_waves: int = 0, peer_halos: bool = False):
     lib = load_library()
     s = (seeds_xy.numel() if hasattr(seeds_xy, "numel") else np.asarray(seeds_xy).size) // 2
     ptr, keep = _addr(seeds_xy, np.uint16, 2 * s)
@@ -186,6 +191,7 @@ def vd_create(N: int, seeds_xy, *, device: int = -1, stream: int | None = None, 
     cfg.metric = METRICS[metric]
     cfg.vn_waves = vn_waves
     cfg.jfa_vn_waves = jfa_vn_waves
+    cfg.peer_halos = 1 if peer_halos else 0
     h = H()
     _check(lib.vd_create(ctypes.byref(h), N, s, ptr, ctypes.byref(cfg)), "vd_create")
     del keep, idbuf
@@ -222,6 +228,28 @@ def vd_djfa_step(h, disp_xy, d_max: int, s: int) -> None:
 def vd_set_labels(h, labels: np.ndarray) -> None:
     arr = np.ascontiguousarray(labels, dtype=np.uint32)
     _check(load_library().vd_set_labels(h, ctypes.c_void_p(arr.ctypes.data)), "vd_set_labels", h)
+
+
+def vd_peer_export(h) -> bytes:
+    lib = load_library()
+    n = ctypes.c_size_t()
+    _check(lib.vd_peer_export(h, None, 0, ctypes.byref(n)), "vd_peer_export", h)
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib.vd_peer_export(h, ctypes.cast(buf, ctypes.c_void_p), n.value, ctypes.byref(n)), "vd_peer_export", h)
+    return buf.raw[:n.value]
+
+
+def vd_peer_attach(h, blobs: list[bytes]) -> None:
+    """blobs: every rank's vd_peer_export() result, in rank order."""
+    each = len(blobs[0])
+    allb = ctypes.create_string_buffer(b"".join(blobs), each * len(blobs))
+    _check(load_library().vd_peer_attach(h, ctypes.cast(allb, ctypes.c_void_p), each), "vd_peer_attach", h)
+
+
+def vd_peer_status(h) -> bool:
+    t = ctypes.c_uint32()
+    _check(load_library().vd_peer_status(h, ctypes.byref(t)), "vd_peer_status", h)
+    return bool(t.value)
 
 
 def vd_pass(h, k: int, von_neumann: bool = False) -> None:
@@ -377,6 +405,17 @@ class VoronoiDiagram:
 
     def set_labels(self, labels):
         vd_set_labels(self.h, labels)
+
+    def attach_peers(self, group=None):
+        """Peer halos across processes: all-gather the IPC blobs over `group` (torch.distributed,
+        any backend) and attach the neighbouring bands (vd_peer_attach)."""
+        import torch.distributed as dist
+        blobs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(blobs, vd_peer_export(self.h), group=group)
+        vd_peer_attach(self.h, blobs)
+
+    def peer_timed_out(self) -> bool:
+        return vd_peer_status(self.h)
 
     def jump_pass(self, k: int, von_neumann: bool = False):
         vd_pass(self.h, k, von_neumann)

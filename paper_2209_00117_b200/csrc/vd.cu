@@ -110,8 +110,8 @@ void halo_plan(uint32_t N, uint32_t world, uint32_t rank, uint32_t k, vd_halo_pl
 struct Shard {
   uint32_t row0 = 0, rows = 0;
   uint32_t* buf[2] = {nullptr, nullptr};  // ping-pong diagrams, rows x pitch
-  uint32_t* top = nullptr;                // halo from the band above, hcap x pitch
-  uint32_t* bot = nullptr;                // halo from the band below
+  uint32_t* top[2] = {nullptr, nullptr};  // halo from the band above, hcap x pitch, by pass parity
+  uint32_t* bot[2] = {nullptr, nullptr};  // halo from the band below
 };
 
 }  // namespace
@@ -159,6 +159,19 @@ struct vd_ctx {
   uint64_t timed_px = 0, timed_launches = 0;
   // NCCL
   ncclComm_t comm = nullptr;
+  // Peer halos (NEXT-3): the pass kernels push the rows the neighbours' next pass needs
+  // straight into their halo buffers (peer memory via CUDA IPC across processes).
+  bool peer = false;           // enabled (vshards: by config; world > 1: after vd_peer_attach)
+  uint32_t hpar = 0;           // halo buffers read by the next pass: top[hpar] / bot[hpar]
+  uint32_t pushed_k = 0;       // the previous pass pushed this step's halos (0: none)
+  uint32_t pass_seq = 0;       // passes run (same on every rank): signal sequence numbers
+  uint32_t* flags = nullptr;   // device u32[2]: seq published by the band above / below
+  uint32_t* peer_err = nullptr;// device u32: a peer wait timed out
+  uint32_t* nbr_bot[2] = {nullptr, nullptr};  // band above's bottom halos (peer pointers)
+  uint32_t* nbr_top[2] = {nullptr, nullptr};  // band below's top halos
+  uint32_t* nbr_flag_above = nullptr;         // band above's flags[1]
+  uint32_t* nbr_flag_below = nullptr;         // band below's flags[0]
+  std::vector<void*> ipc_opened;
 };
 
 namespace {
@@ -298,13 +311,26 @@ bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 
 bool rel_ok(uint32_t N, bool may_empty, uint32_t k) { return !may_empty && !fast_ok(N, false) && k <= 4096; }
 
 // One pass over output rows [y_lo, y_hi) of shard sh (global rows; default: the whole band).
+struct Push {  // where a launch also stores the rows the neighbours' next pass needs
+  uint32_t* top = nullptr;
+  uint32_t* bot = nullptr;
+  uint32_t k = 0;
+};
+
 vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn, int64_t y_lo = -1,
-                      int64_t y_hi = -1) {
+                      int64_t y_hi = -1, const Push* push = nullptr) {
   vdk::PassArgs a;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
-  a.top = sh.top;
-  a.bot = sh.bot;
+  a.top = sh.top[h->hpar];
+  a.bot = sh.bot[h->hpar];
+  a.push_top = a.push_bot = nullptr;
+  a.push_k = 0;
+  if (push && push->k) {
+    a.push_top = push->top;
+    a.push_bot = push->bot;
+    a.push_k = (int)push->k;
+  }
   a.pitch = h->pitch;
   a.N = (int)h->N;
   a.row0 = (int)sh.row0;
@@ -336,7 +362,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
-    const bool banded = sh.top != nullptr;
+    const bool banded = sh.top[0] != nullptr;
     const size_t sm = vdk::pass_smem((int)k, rel);
     cudaError_t e;
     if (k == 1) e = launch_fast_k<1>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
@@ -375,11 +401,11 @@ vd_status exchange_halos(vd_ctx* h, uint32_t k, cudaStream_t st) {
     const size_t cnt = (size_t)p.halo_rows * h->pitch;
     CKN(g_nccl.GroupStart());
     if (p.recv_top_rank >= 0) {
-      CKN(g_nccl.Recv(sh.top, cnt, ncclUint32, p.recv_top_rank, h->comm, st));
+      CKN(g_nccl.Recv(sh.top[h->hpar], cnt, ncclUint32, p.recv_top_rank, h->comm, st));
       CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_top_row0 * h->pitch, cnt, ncclUint32, p.recv_top_rank, h->comm, st));
     }
     if (p.recv_bot_rank >= 0) {
-      CKN(g_nccl.Recv(sh.bot, cnt, ncclUint32, p.recv_bot_rank, h->comm, st));
+      CKN(g_nccl.Recv(sh.bot[h->hpar], cnt, ncclUint32, p.recv_bot_rank, h->comm, st));
       CKN(g_nccl.Send(sh.buf[h->cur] + (size_t)p.send_bot_row0 * h->pitch, cnt, ncclUint32, p.recv_bot_rank, h->comm, st));
     }
     CKN(g_nccl.GroupEnd());
@@ -389,37 +415,64 @@ vd_status exchange_halos(vd_ctx* h, uint32_t k, cudaStream_t st) {
       halo_plan(h->N, h->vshards, g, k, p);
       Shard& sh = h->shards[g];
       if (p.recv_top_rank >= 0)
-        CK(cudaMemcpyAsync(sh.top, h->shards[p.recv_top_rank].buf[h->cur] + (size_t)(sh.rows - p.halo_rows) * h->pitch,
+        CK(cudaMemcpyAsync(sh.top[h->hpar], h->shards[p.recv_top_rank].buf[h->cur] + (size_t)(sh.rows - p.halo_rows) * h->pitch,
                            p.halo_rows * row_bytes, cudaMemcpyDeviceToDevice, st));
       if (p.recv_bot_rank >= 0)
-        CK(cudaMemcpyAsync(sh.bot, h->shards[p.recv_bot_rank].buf[h->cur], p.halo_rows * row_bytes,
+        CK(cudaMemcpyAsync(sh.bot[h->hpar], h->shards[p.recv_bot_rank].buf[h->cur], p.halo_rows * row_bytes,
                            cudaMemcpyDeviceToDevice, st));
     }
   }
   return VD_OK;
 }
 
-// One pass on every shard.  Sharded with k < B/2: the halos travel on halo_stream while the
+// One pass on every shard.  Sharded with 2k < B: the halos travel on halo_stream while the
 // interior rows [k, B-k) of each band, which read no halo, are computed; then the two edge
 // strips ("compute interior rows while the halos are in flight").
-vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
+// Peer halos (h->peer, NEXT-3): the edge strips also store the rows the neighbours' next pass
+// (step k_next) reads straight into their halo buffers, so that pass needs no exchange; across
+// processes a flag in the neighbour's memory announces them (peer_signal / peer_wait).
+vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false, uint32_t k_next = 0) {
   vd_status st;
   const bool sharded = h->world > 1 || h->vshards > 1;
-  const bool overlap = sharded && 2 * k < h->shards[0].rows;
+  const uint32_t B = h->shards[0].rows;
+  const bool overlap = sharded && 2 * k < B;
+  const uint32_t seq = ++h->pass_seq;
+  const bool multi_peer = h->peer && h->world > 1;
   if (!overlap) {
-    if (sharded && (st = exchange_halos(h, k, h->stream))) return st;
+    if (sharded) {
+      if (h->world > 1 && !h->comm) return fail(h, VD_ERR_STATE, "step %u needs the NCCL exchange (no communicator)", k);
+      if ((st = exchange_halos(h, k, h->stream))) return st;
+    }
     for (auto& sh : h->shards) {
       if ((st = timed_begin(h))) return st;
       if ((st = launch_pass(h, sh, k, may_empty, vn))) return st;
       if ((st = timed_end(h, (uint64_t)sh.rows * h->N))) return st;
     }
+    h->pushed_k = 0;
+    h->hpar ^= 1;
     h->cur ^= 1;
     return VD_OK;
   }
-  CK(cudaEventRecord(h->halo_ready, h->stream));  // this pass's input is complete
-  CK(cudaStreamWaitEvent(h->halo_stream, h->halo_ready, 0));
-  if ((st = exchange_halos(h, k, h->halo_stream))) return st;
-  CK(cudaEventRecord(h->halo_done, h->halo_stream));
+  const bool have = h->peer && h->pushed_k == k;  // the previous pass pushed this pass's halos
+  const bool push_next = h->peer && k_next > 0 && 2 * k_next < B && k_next <= h->hcap;
+  const bool has_above = h->rank > 0, has_below = h->rank + 1 < h->world;
+  if (!have) {
+    CK(cudaEventRecord(h->halo_ready, h->stream));  // this pass's input is complete
+    CK(cudaStreamWaitEvent(h->halo_stream, h->halo_ready, 0));
+    if (multi_peer) {  // copy the edge rows into the neighbours' halos, then announce them
+      const Shard& sh = h->shards[0];
+      const int64_t n4 = (int64_t)k * (h->pitch / 4);
+      vdk::push_rows<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 8), 256, 0, h->halo_stream>>>(
+          sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, (int)k, has_above ? h->nbr_bot[h->hpar] : nullptr,
+          has_below ? h->nbr_top[h->hpar] : nullptr);
+      if ((st = after_launch(h, "push_rows"))) return st;
+      vdk::peer_signal<<<1, 1, 0, h->halo_stream>>>(h->nbr_flag_above, h->nbr_flag_below, seq);
+      if ((st = after_launch(h, "peer_signal"))) return st;
+    } else if ((st = exchange_halos(h, k, h->halo_stream))) {
+      return st;
+    }
+    CK(cudaEventRecord(h->halo_done, h->halo_stream));
+  }
   // one timed interval per pass: first interior launch .. last edge strip
   if ((st = timed_begin(h))) return st;
   uint64_t px = 0;
@@ -428,13 +481,36 @@ vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false) {
     if ((st = launch_pass(h, sh, k, may_empty, vn, r0 + k, r1 - k))) return st;
     px += (uint64_t)sh.rows * h->N;
   }
-  CK(cudaStreamWaitEvent(h->stream, h->halo_done, 0));
-  for (auto& sh : h->shards) {
+  if (!have) CK(cudaStreamWaitEvent(h->stream, h->halo_done, 0));
+  if (multi_peer) {
+    vdk::peer_wait<<<1, 1, 0, h->stream>>>(h->flags, has_above, has_below, seq, h->peer_err);
+    if ((st = after_launch(h, "peer_wait"))) return st;
+  }
+  const uint32_t nxt = h->hpar ^ 1;
+  for (size_t g = 0; g < h->shards.size(); ++g) {
+    Shard& sh = h->shards[g];
+    Push push;
+    if (push_next) {
+      push.k = k_next;
+      if (h->world > 1) {
+        push.top = has_above ? h->nbr_bot[nxt] : nullptr;
+        push.bot = has_below ? h->nbr_top[nxt] : nullptr;
+      } else {
+        push.top = g > 0 ? h->shards[g - 1].bot[nxt] : nullptr;
+        push.bot = g + 1 < h->shards.size() ? h->shards[g + 1].top[nxt] : nullptr;
+      }
+    }
     const int64_t r0 = (int64_t)sh.row0, r1 = r0 + (int64_t)sh.rows;
-    if ((st = launch_pass(h, sh, k, may_empty, vn, r0, r0 + k))) return st;  // top strip
-    if ((st = launch_pass(h, sh, k, may_empty, vn, r1 - k, r1))) return st;  // bottom strip
+    if ((st = launch_pass(h, sh, k, may_empty, vn, r0, r0 + k, &push))) return st;  // top strip
+    if ((st = launch_pass(h, sh, k, may_empty, vn, r1 - k, r1, &push))) return st;  // bottom strip
+  }
+  if (multi_peer && push_next) {
+    vdk::peer_signal<<<1, 1, 0, h->stream>>>(h->nbr_flag_above, h->nbr_flag_below, seq + 1);
+    if ((st = after_launch(h, "peer_signal"))) return st;
   }
   if ((st = timed_end(h, px))) return st;
+  h->pushed_k = push_next ? k_next : 0;
+  h->hpar ^= 1;
   h->cur ^= 1;
   return VD_OK;
 }
@@ -463,6 +539,7 @@ vd_status move_seeds(vd_ctx* h, const int16_t* disp_xy) {
 
 vd_status reduce_to_host(vd_ctx* h, uint64_t* out) {
   if (h->world > 1) {
+    if (!h->comm) return fail(h, VD_ERR_STATE, "no NCCL communicator for the cross-rank sum");
     CKN(g_nccl.AllReduce(h->counter, h->counter, 1, ncclUint64, ncclSum, h->comm, h->stream));
   }
   CK(cudaMemcpyAsync(h->counter_h, h->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
@@ -487,9 +564,15 @@ void free_all(vd_ctx* h) {
   for (auto& sh : h->shards) {
     cudaFree(sh.buf[0]);
     cudaFree(sh.buf[1]);
-    cudaFree(sh.top);
-    cudaFree(sh.bot);
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(sh.top[i]);
+      cudaFree(sh.bot[i]);
+    }
   }
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  h->ipc_opened.clear();
+  cudaFree(h->flags);
+  cudaFree(h->peer_err);
   h->shards.clear();
   cudaFree(h->seeds);
   cudaFree(h->seeds_new);
@@ -621,9 +704,10 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   const uint32_t G = cfg.world > 1 ? (uint32_t)cfg.world : vsh;
   if (cfg.world > 1 && vsh > 1) return VD_ERR_ARG;
   if (G > 1 && (!pow2 || N % G != 0 || (G & (G - 1)) != 0)) return VD_ERR_ARG;
-  if (cfg.world > 1 && !cfg.nccl_id) return VD_ERR_ARG;
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 2; ++i)
     if (cfg.reserved[i]) return VD_ERR_ARG;
+  if (cfg.peer_halos > 1) return VD_ERR_ARG;
+  if (cfg.world > 1 && !cfg.nccl_id && !cfg.peer_halos) return VD_ERR_ARG;
   if (cfg.metric > 1) return VD_ERR_ARG;
 
   // Validate and pack the seeds on the host (R-1, R-4).
@@ -700,10 +784,12 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
     CKC(cudaMemsetAsync(r.buf[1], 0xFF, bytes, h->stream));
     if (h->hcap) {
       const size_t hb = (size_t)h->hcap * h->pitch * sizeof(uint32_t);
-      CKC(cudaMalloc(&r.top, hb));
-      CKC(cudaMalloc(&r.bot, hb));
-      CKC(cudaMemsetAsync(r.top, 0xFF, hb, h->stream));
-      CKC(cudaMemsetAsync(r.bot, 0xFF, hb, h->stream));
+      for (int i = 0; i < 2; ++i) {
+        CKC(cudaMalloc(&r.top[i], hb));
+        CKC(cudaMalloc(&r.bot[i], hb));
+        CKC(cudaMemsetAsync(r.top[i], 0xFF, hb, h->stream));
+        CKC(cudaMemsetAsync(r.bot[i], 0xFF, hb, h->stream));
+      }
     }
   }
   CKC(cudaMalloc(&h->seeds, s * sizeof(uint32_t)));
@@ -720,10 +806,15 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
     CKC(cudaEventRecord(e, h->stream));
   }
   CKC(cudaMalloc(&h->counter, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->flags, 2 * sizeof(uint32_t)));
+  CKC(cudaMemset(h->flags, 0, 2 * sizeof(uint32_t)));
+  CKC(cudaMalloc(&h->peer_err, sizeof(uint32_t)));
+  CKC(cudaMemset(h->peer_err, 0, sizeof(uint32_t)));
+  h->peer = cfg.peer_halos && cfg.world == 1 && h->vshards > 1;  // across processes: vd_peer_attach
   CKC(cudaMallocHost(&h->counter_h, sizeof(unsigned long long)));
   CKC(cudaMemcpyAsync(h->seeds, packed.data(), s * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
   CKC(cudaStreamSynchronize(h->stream));
-  if (cfg.world > 1) {
+  if (cfg.world > 1 && cfg.nccl_id) {
     if (!nccl_load()) return bail(VD_ERR_NCCL);
     ncclUniqueId id;
     memcpy(&id, cfg.nccl_id, sizeof id);
@@ -764,7 +855,7 @@ vd_status vd_jfa(vd_handle h) {
     // JFA's labels are still far from their pixels at large steps: there the windowed kernel
     // would recompute most walks, and the 64-bit one is cheaper (C5: 31 vs 68 ms at k = 512).
     const bool far = h->N > 32768 && ks[i] > 256;
-    st = run_pass(h, ks[i], may_empty || far, vn);
+    st = run_pass(h, ks[i], may_empty || far, vn, i + 1 < ks.size() ? ks[i + 1] : 0);
     h->track_empty = false;
     if (st) return st;
     if (track && may_empty) {
@@ -868,7 +959,7 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   // 4. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
   //    seed), so no EMPTY exists.
   for (size_t i = 0; i < ks.size(); ++i)
-    if ((st = run_pass(h, ks[i], false, i < h->vn_waves))) return st;
+    if ((st = run_pass(h, ks[i], false, i < h->vn_waves, i + 1 < ks.size() ? ks[i + 1] : 0))) return st;
   h->last_passes = (uint32_t)ks.size();
   return VD_OK;
 }
@@ -911,6 +1002,82 @@ vd_status vd_pass(vd_handle h, uint32_t k, uint32_t flags) {
   // pass, so the EMPTY-free kernels apply; across ranks completeness is not known globally.
   const bool may_empty = !h->has_diagram || h->world > 1;
   return run_pass(h, k, may_empty, (flags & VD_PASS_VON_NEUMANN) != 0);
+}
+
+// ---- peer halos across processes (NEXT-3) ----
+namespace {
+struct PeerBlob {
+  int32_t rank, world;
+  uint32_t N, hcap;
+  cudaIpcMemHandle_t top[2], bot[2], flags;
+};
+}  // namespace
+
+vd_status vd_peer_export(vd_handle h, void* out, size_t cap, size_t* len) {
+  CHECK_HANDLE(h);
+  if (len) *len = sizeof(PeerBlob);
+  if (!out) return len ? VD_OK : VD_ERR_ARG;
+  if (cap < sizeof(PeerBlob)) return VD_ERR_ARG;
+  if (h->world < 2) return fail(h, VD_ERR_STATE, "vd_peer_export needs world > 1");
+  DeviceGuard guard(h->device);
+  PeerBlob b{};
+  b.rank = h->rank;
+  b.world = h->world;
+  b.N = h->N;
+  b.hcap = h->hcap;
+  const Shard& sh = h->shards[0];
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaIpcGetMemHandle(&b.top[i], sh.top[i]));
+    CK(cudaIpcGetMemHandle(&b.bot[i], sh.bot[i]));
+  }
+  CK(cudaIpcGetMemHandle(&b.flags, h->flags));
+  memcpy(out, &b, sizeof b);
+  return VD_OK;
+}
+
+vd_status vd_peer_attach(vd_handle h, const void* blobs, size_t len_each) {
+  CHECK_HANDLE(h);
+  if (!blobs || len_each != sizeof(PeerBlob)) return VD_ERR_ARG;
+  if (h->world < 2 || h->peer) return fail(h, VD_ERR_STATE, "vd_peer_attach: needs world > 1, once");
+  DeviceGuard guard(h->device);
+  const auto* all = static_cast<const PeerBlob*>(blobs);
+  for (int r = 0; r < h->world; ++r)
+    if (all[r].rank != r || all[r].world != h->world || all[r].N != h->N || all[r].hcap != h->hcap)
+      return fail(h, VD_ERR_ARG, "vd_peer_attach: blob %d does not match this grid", r);
+  auto open = [&](const cudaIpcMemHandle_t& hd, uint32_t** out) -> vd_status {
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_opened.push_back(p);
+    *out = static_cast<uint32_t*>(p);
+    return VD_OK;
+  };
+  vd_status st;
+  uint32_t* f = nullptr;
+  if (h->rank > 0) {  // the band above: its bottom halos and its "from below" flag
+    const PeerBlob& b = all[h->rank - 1];
+    for (int i = 0; i < 2; ++i)
+      if ((st = open(b.bot[i], &h->nbr_bot[i]))) return st;
+    if ((st = open(b.flags, &f))) return st;
+    h->nbr_flag_above = f + 1;
+  }
+  if (h->rank + 1 < h->world) {  // the band below: its top halos and its "from above" flag
+    const PeerBlob& b = all[h->rank + 1];
+    for (int i = 0; i < 2; ++i)
+      if ((st = open(b.top[i], &h->nbr_top[i]))) return st;
+    if ((st = open(b.flags, &f))) return st;
+    h->nbr_flag_below = f;
+  }
+  h->peer = true;
+  return VD_OK;
+}
+
+vd_status vd_peer_status(vd_handle h, uint32_t* timed_out) {
+  CHECK_HANDLE(h);
+  if (!timed_out) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(timed_out, h->peer_err, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return VD_OK;
 }
 
 vd_status vd_similarity(vd_handle h, vd_handle ref, double* pct, uint64_t* matches) {

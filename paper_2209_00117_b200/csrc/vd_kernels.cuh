@@ -48,7 +48,27 @@ struct PassArgs {
   int32_t metric;   // 0 Euclidean, 1 Manhattan (jump_pass_wide; the fast kernel templates it)
   int32_t vn;       // Von Neumann neighbourhood (jump_pass_wide)
   unsigned long long* empty_flag;  // jump_pass_wide: set non-zero if any output is EMPTY (or null)
+  // Fused halo push (peer halos, NEXT-3): output rows [row0, row0 + push_k) are also stored
+  // into the band above's bottom halo (push_top, row y at y - row0) and rows
+  // [row0 + rows - push_k, row0 + rows) into the band below's top halo (push_bot, row y at
+  // y - (row0 + rows - push_k)); peer memory when the bands live on other GPUs.
+  uint32_t* push_top;
+  uint32_t* push_bot;
+  int32_t push_k;
 };
+
+// Store one output vector of row y (band-local pointer po) and, for the rows a neighbour's
+// next pass reads as halo, the same vector into its halo buffer.
+template <typename V>
+__device__ __forceinline__ void store_out(const PassArgs& a, bool banded, int y, int x, uint32_t* po, const V& v) {
+  *reinterpret_cast<V*>(po) = v;
+  if (banded && a.push_k) {
+    if (a.push_top && y < a.row0 + a.push_k)
+      *reinterpret_cast<V*>(a.push_top + (int64_t)(y - a.row0) * a.pitch + x) = v;
+    const int b0 = a.row0 + a.rows - a.push_k;
+    if (a.push_bot && y >= b0) *reinterpret_cast<V*>(a.push_bot + (int64_t)(y - b0) * a.pitch + x) = v;
+  }
+}
 
 __device__ __forceinline__ const uint32_t* row_ptr(const PassArgs& a, int r) {
   if (r >= a.row0 && r < a.row0 + a.rows) return a.in + (int64_t)(r - a.row0) * a.pitch;
@@ -388,8 +408,8 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
       o[e] = v;
     }
     if (active) {
-      if constexpr (kVec == 4) *reinterpret_cast<uint4*>(po) = make_uint4(o[0], o[1], o[2], o[3]);
-      else *reinterpret_cast<uint2*>(po) = make_uint2(o[0], o[1]);
+      if constexpr (kVec == 4) store_out(a, BANDED, y, x, po, make_uint4(o[0], o[1], o[2], o[3]));
+      else store_out(a, BANDED, y, x, po, make_uint2(o[0], o[1]));
     }
     po += kp;
     y += k;
@@ -430,8 +450,8 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
         }
         if (active) {
           uint32_t* pw = a.out + (int64_t)(yy - a.row0) * a.pitch + x;
-          if constexpr (kVec == 4) *reinterpret_cast<uint4*>(pw) = make_uint4(o[0], o[1], o[2], o[3]);
-          else *reinterpret_cast<uint2*>(pw) = make_uint2(o[0], o[1]);
+          if constexpr (kVec == 4) store_out(a, BANDED, yy, x, pw, make_uint4(o[0], o[1], o[2], o[3]));
+          else store_out(a, BANDED, yy, x, pw, make_uint2(o[0], o[1]));
         }
       }
     }
@@ -511,10 +531,50 @@ __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) any_empty |= (x + e < N) && best[e] == EMPTY;
     // columns >= N of the ragged tail hold don't-care values (never read as pixels)
-    *reinterpret_cast<uint4*>(a.out + (int64_t)(y - a.row0) * a.pitch + x) =
-        make_uint4(best[0], best[1], best[2], best[3]);
+    store_out(a, true, y, x, a.out + (int64_t)(y - a.row0) * a.pitch + x, make_uint4(best[0], best[1], best[2], best[3]));
   }
   if (a.empty_flag != nullptr && __syncthreads_or(any_empty) && threadIdx.x == 0) atomicOr(a.empty_flag, 1ull);
+}
+
+// ------------------------------------------------------------------ peer halos (NEXT-3)
+// Copy this band's first / last k rows into the neighbours' halo buffers (the first pass of
+// a sequence; later passes push from inside the pass kernel, store_out).
+__global__ void push_rows(const uint32_t* __restrict__ band, int64_t pitch, int rows, int N, int k,
+                          uint32_t* __restrict__ to_top, uint32_t* __restrict__ to_bot) {
+  const int64_t n4 = (int64_t)k * (pitch / 4);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (pitch / 4), c = (i % (pitch / 4)) * 4;
+    if (c >= N) continue;
+    if (to_top) *reinterpret_cast<uint4*>(to_top + r * pitch + c) = *reinterpret_cast<const uint4*>(band + r * pitch + c);
+    if (to_bot)
+      *reinterpret_cast<uint4*>(to_bot + r * pitch + c) =
+          *reinterpret_cast<const uint4*>(band + (int64_t)(rows - k + r) * pitch + c);
+  }
+}
+
+// After this rank's pushes for the neighbours' next pass: make them visible system-wide,
+// then publish `seq` into each neighbour's flag word (its flags[1] = "from the band above",
+// flags[0] = "from the band below").
+__global__ void peer_signal(uint32_t* flag_top_nbr, uint32_t* flag_bot_nbr, uint32_t seq) {
+  __threadfence_system();
+  if (flag_top_nbr) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_top_nbr), "r"(seq) : "memory");
+  if (flag_bot_nbr) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_bot_nbr), "r"(seq) : "memory");
+}
+
+// Wait until the neighbours published `seq` (their pushes into this rank's halos landed).
+// Bounded: after ~20 s it records an error instead of hanging the GPU.
+__global__ void peer_wait(const uint32_t* flags, int need_top, int need_bot, uint32_t seq, uint32_t* err) {
+  for (int side = 0; side < 2; ++side) {
+    if (!(side == 0 ? need_top : need_bot)) continue;
+    const uint32_t* f = flags + side;
+    for (long long it = 0;; ++it) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if ((int32_t)(v - seq) >= 0) break;
+      if (it > (1ll << 24)) { atomicExch(err, 1u); return; }
+      __nanosleep(1000);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ JFA init
@@ -690,23 +750,26 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 // (p = global y*N + x < 2^32).
 __global__ void label_hash(const uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N,
                            unsigned long long* __restrict__ out) {
+  // sum over p of fmix32(p * 0x9E3779B9 ^ label[p]) mod 2^64 (p = y * N + x).  The position
+  // term advances by a constant per column, so it costs one add per pixel.
+  constexpr uint32_t C = 0x9E3779B9u;
   uint64_t h = 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const uint32_t* row = g + (int64_t)r * pitch;
-    const uint32_t p0 = (uint32_t)(row0 + r) * (uint32_t)N;
+    const uint32_t pc0 = (uint32_t)(row0 + r) * (uint32_t)N * C;
 #pragma unroll 4
     for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + x));
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-      uint32_t acc = 0, carry = 0;
+      const uint32_t b = pc0 + (uint32_t)x * C;
+      if (x + 3 < N) {
+        h += (uint64_t)fmix32(b ^ u.x) + fmix32((b + C) ^ u.y);
+        h += (uint64_t)fmix32((b + 2 * C) ^ u.z) + fmix32((b + 3 * C) ^ u.w);
+      } else {
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (x + e < N) {
-          const uint32_t m = fmix32((p0 + (uint32_t)(x + e)) * 0x9E3779B9u ^ w[e]);
-          acc += m;
-          carry += acc < m;
-        }
-      h += ((uint64_t)carry << 32) | acc;
+        for (int e = 0; e < 4; ++e)
+          if (x + e < N) h += fmix32((b + (uint32_t)e * C) ^ w[e]);
+      }
     }
   }
   uint64_t t = block_sum_u64(h);

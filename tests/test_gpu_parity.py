@@ -482,3 +482,68 @@ def test_windowed_pass_full_c5_size_bit_exact(vd):
         assert np.array_equal(got, want), k
         del got, want
     d.close()
+
+
+# ---------------------------------------------------------------- peer halos (NEXT-3)
+
+@pytest.mark.parametrize("G,metric,vn_waves", [(2, "euclid", 0), (4, "euclid", 2), (8, "manhattan", 0)])
+def test_peer_halos_virtual_shards_bit_exact(vd, G, metric, vn_waves):
+    # Halo rows pushed by the pass kernels into the neighbouring bands' (double-buffered)
+    # halo buffers instead of exchanged before each pass: JFA + dJFA identical to the oracle.
+    N, s, dmax = 1024, 1024, 2
+    xy = synth.uniform_seeds(N, s, rng_seed=G + 40)
+    d = _jfa_gpu(vd, N, xy, metric=metric, vn_waves=vn_waves, virtual_shards=G, peer_halos=True)
+    ref = oracle.jfa(N, xy, metric=metric)
+    assert np.array_equal(d.labels(), ref)
+    for f in range(4):
+        disp = synth.displacements(s, dmax, f, rng_seed=G)
+        d.djfa_step(disp, dmax)
+        ref, xy, _ = oracle.djfa_step(N, xy, disp, dmax, ref, metric=metric, vn_waves=vn_waves)
+        assert np.array_equal(d.labels(), ref), f
+
+
+def _peer_worker(rank, world, port, N, s, dmax, frames, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2209_00117_b200 as m
+    m.load_library()
+    xy = synth.uniform_seeds(N, s, rng_seed=5)
+    ref = oracle.jfa(N, xy)
+    B = N // world
+    d = m.VoronoiDiagram(N, xy, device=0, rank=rank, world=world, peer_halos=True)  # no NCCL id
+    d.attach_peers()
+    d.set_labels(ref[rank * B:(rank + 1) * B])
+    ok = True
+    for f in range(frames):
+        disp = synth.displacements(s, dmax, f, rng_seed=5)
+        d.djfa_step(disp, dmax)
+        ref, xy, _ = oracle.djfa_step(N, xy, disp, dmax, ref)
+        ok &= bool(np.array_equal(d.labels(), ref[rank * B:(rank + 1) * B]))
+    q.put((rank, ok, d.peer_timed_out()))
+    dist.barrier()
+    d.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_halos_two_processes_one_gpu(vd, world):
+    # The cross-process path: each rank a process (here all on cuda:0), IPC-mapped halo buffers
+    # and flag words, fused pushes + release/acquire flags, no NCCL communicator at all.
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_peer_worker, args=(r, world, port, 512, 1024, 2, 3, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(timeout=120)
+    assert [r for r, _, _ in res] == list(range(world))
+    assert all(ok for _, ok, _ in res), res
+    assert not any(t for _, _, t in res), res
