@@ -359,6 +359,14 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     const uint32_t per_res = (R + k - 1) / k;
     a.walk = vdk::walk_len((int)k, rel);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
+    // Small grids (C2: 1024^2 at k = 1 is 2 x 1 x 43 walks of 24 rows): shorten the walks until
+    // there are about two waves of resident CTAs, else a few long walks leave SMs idle.
+    const int64_t base = (int64_t)a.xblocks * nres;
+    const int64_t want = (int64_t)h->num_sms * 8;
+    if (base * (int64_t)((per_res + a.walk - 1) / a.walk) < want) {
+      const int64_t segs_want = (want + base - 1) / base;
+      a.walk = (int)std::max<int64_t>(2, std::min<int64_t>(a.walk, ((int64_t)per_res + segs_want - 1) / segs_want));
+    }
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
