@@ -181,6 +181,11 @@ vd_status vd_similarity_host(vd_handle h, const uint32_t* ref_labels, double* pc
  * finaliser; summed over ranks when world > 1).  Reads the whole diagram once and returns
  * 8 bytes; used as the per-step result read-back. */
 vd_status vd_label_hash(vd_handle h, uint64_t* out);
+/* Same checksum, enqueued on the handle's stream without waiting: the value lands in
+ * *pinned_out (page-locked host memory: cudaHostAlloc / cudaHostRegister / torch pin_memory)
+ * once the stream reaches it, i.e. after vd_synchronize or any later synchronising call. Lets
+ * a time-stepping loop read each step's result without a host round trip per step. */
+vd_status vd_label_hash_async(vd_handle h, uint64_t* pinned_out);
 
 /* Copy the diagram to host: N*N labels (world = 1, any virtual_shards), or this rank's
  * band_rows*N labels (world > 1). */

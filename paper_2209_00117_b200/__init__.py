@@ -25,7 +25,7 @@ __all__ = [
     "vd_get_seeds", "vd_band", "vd_last_passes", "vd_synchronize", "vd_set_pass_timing",
     "vd_pass_timing", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
     "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "vd_peer_export",
-    "vd_peer_attach", "vd_peer_status", "EXPORTED_SYMBOLS",
+    "vd_peer_attach", "vd_peer_status", "vd_label_hash_async", "EXPORTED_SYMBOLS",
 ]
 
 EMPTY = 0xFFFFFFFF
@@ -86,6 +86,7 @@ _SIGS = {
     "vd_similarity": (ctypes.c_int32, [H, H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "vd_similarity_host": (ctypes.c_int32, [H, P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "vd_label_hash": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint64)]),
+    "vd_label_hash_async": (ctypes.c_int32, [H, P]),
     "vd_get_labels": (ctypes.c_int32, [H, P]),
     "vd_get_seeds": (ctypes.c_int32, [H, P]),
     "vd_band": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
@@ -274,6 +275,11 @@ def vd_label_hash(h) -> int:
     v = ctypes.c_uint64()
     _check(load_library().vd_label_hash(h, ctypes.byref(v)), "vd_label_hash", h)
     return v.value
+
+
+def vd_label_hash_async(h, pinned_ptr: int) -> None:
+    """Enqueue the checksum; it lands at pinned_ptr (page-locked host memory) asynchronously."""
+    _check(load_library().vd_label_hash_async(h, ctypes.c_void_p(pinned_ptr)), "vd_label_hash_async", h)
 
 
 def vd_band(h) -> tuple[int, int]:

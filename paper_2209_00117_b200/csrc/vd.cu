@@ -1139,10 +1139,8 @@ vd_status vd_similarity_host(vd_handle h, const uint32_t* ref_labels, double* pc
   return VD_OK;
 }
 
-vd_status vd_label_hash(vd_handle h, uint64_t* out) {
-  CHECK_HANDLE(h);
-  if (!out) return VD_ERR_ARG;
-  DeviceGuard guard(h->device);
+namespace {
+vd_status enqueue_label_hash(vd_ctx* h) {
   CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
   for (auto& sh : h->shards) {
     vdk::label_hash<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
@@ -1150,7 +1148,31 @@ vd_status vd_label_hash(vd_handle h, uint64_t* out) {
     vd_status st = after_launch(h, "label_hash");
     if (st) return st;
   }
+  return VD_OK;
+}
+}  // namespace
+
+vd_status vd_label_hash(vd_handle h, uint64_t* out) {
+  CHECK_HANDLE(h);
+  if (!out) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  vd_status st = enqueue_label_hash(h);
+  if (st) return st;
   return reduce_to_host(h, out);
+}
+
+vd_status vd_label_hash_async(vd_handle h, uint64_t* pinned_out) {
+  CHECK_HANDLE(h);
+  if (!pinned_out) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  vd_status st = enqueue_label_hash(h);
+  if (st) return st;
+  if (h->world > 1) {
+    if (!h->comm) return fail(h, VD_ERR_STATE, "no NCCL communicator for the cross-rank sum");
+    CKN(g_nccl.AllReduce(h->counter, h->counter, 1, ncclUint64, ncclSum, h->comm, h->stream));
+  }
+  CK(cudaMemcpyAsync(pinned_out, h->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+  return VD_OK;
 }
 
 vd_status vd_get_labels(vd_handle h, uint32_t* out) {

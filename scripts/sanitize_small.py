@@ -11,6 +11,7 @@ import paper_2209_00117_b200 as vd  # noqa: E402
 cases = [
     (64, 16, {}), (1031, 200, {}), (1024, 1024, {}), (256, 100, {"virtual_shards": 4}),
     (300, 50, {"metric": "manhattan", "vn_waves": 2}), (128, 30, {"jfa_vn_waves": 99}),
+    (1024, 1024, {"virtual_shards": 4, "peer_halos": True}), (512, 300, {"virtual_shards": 2, "peer_halos": True}),
 ]
 for N, s, cfg in cases:
     xy = synth.uniform_seeds(N, s, rng_seed=1)
@@ -28,3 +29,19 @@ for N, s, cfg in cases:
     print(N, s, cfg, hex(d.label_hash()), d.match_count(d), flush=True)
     d.close()
     e.close()
+
+# the windowed kernel (forced at small N) on a complete map, including its exact recomputation
+os.environ["VD_FORCE_WINDOWED"] = "1"
+N, s = 1031, 300
+xy = synth.uniform_seeds(N, s, rng_seed=2)
+d = vd.VoronoiDiagram(N, xy)
+d.jfa()
+for f in range(2):
+    d.djfa_step(synth.displacements(s, 3, f, rng_seed=2), 3)
+G = d.labels()
+rng = np.random.default_rng(0)
+for k in (1, 2, 4, 16, 512):
+    d.set_labels(G)
+    d.jump_pass(k)
+print("windowed", hex(d.label_hash()), flush=True)
+d.close()

@@ -547,3 +547,20 @@ def test_peer_halos_two_processes_one_gpu(vd, world):
     assert [r for r, _, _ in res] == list(range(world))
     assert all(ok for _, ok, _ in res), res
     assert not any(t for _, _, t in res), res
+
+
+def test_label_hash_async_matches(vd):
+    N, s = 512, 300
+    xy = synth.uniform_seeds(N, s, rng_seed=9)
+    d = _jfa_gpu(vd, N, xy, virtual_shards=2)
+    out = torch.zeros(3, dtype=torch.int64).pin_memory()
+    ref = oracle.jfa(N, xy)
+    want = []
+    for f in range(3):
+        disp = synth.displacements(s, 2, f, rng_seed=9)
+        d.djfa_step(disp, 2)
+        vd.vd_label_hash_async(d.h, out[f].data_ptr())
+        ref, xy, _ = oracle.djfa_step(N, xy, disp, 2, ref)
+        want.append(oracle.label_hash(ref))
+    d.synchronize()
+    assert [int(v) & 0xFFFFFFFFFFFFFFFF for v in out] == want
