@@ -368,8 +368,9 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
       a.walk = (int)std::max<int64_t>(2, std::min<int64_t>(a.walk, ((int64_t)per_res + segs_want - 1) / segs_want));
     }
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
-    const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
-    const dim3 grid((unsigned)blocks), blk(vdk::kThreads);
+    a.lk = 0;
+    while ((1u << a.lk) < k) ++a.lk;
+    const dim3 grid((unsigned)a.xblocks, (unsigned)a.segs, nres), blk(vdk::kThreads);
     const bool banded = sh.top[0] != nullptr;
     const size_t sm = vdk::pass_smem((int)k, rel);
     cudaError_t e;

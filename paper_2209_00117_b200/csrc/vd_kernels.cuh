@@ -39,6 +39,7 @@ struct PassArgs {
   int32_t N, row0, rows, top_row0, bot_row0, k;
   int32_t y_lo, y_hi;  // output rows [y_lo, y_hi) (global), inside the band: the whole band, or the
                        // interior / an edge strip when the halo exchange is overlapped
+  int32_t lk;       // log2(k) (fast pass: k is a power of two)
   int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / walk)
   int32_t walk;     // output rows per walk (walk_len(k))
   int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
@@ -197,6 +198,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// One lane of the (converged) warp: elect.sync.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n .reg .b32 r;\n .reg .pred p;\n elect.sync r|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(e));
+  return e != 0u;
+}
+
 template <int V>
 struct VecT;
 template <>
@@ -324,7 +334,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   const int tid = (int)threadIdx.x;
   const int x = x0 + kVec * tid;
   const int yend = a.y_hi;
-  const int nout = min(a.walk, (yend - y0 + k - 1) / k);  // output rows of this walk
+  const int nout = min(a.walk, (yend - y0 + k - 1) >> a.lk);  // output rows of this walk (k = 2^lk)
   const int nlist = nout + 2;                              // staged input rows
   const bool spans3 = k >= kW;
   const int K4 = (k + 3) & ~3;
@@ -334,28 +344,33 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   if (tid < nlist) mbar_init(&bars[tid], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();  // barrier initialisation visible to every thread (and to the async proxy)
-  if ((tid & 31) == 0) {  // lane 0 of each warp issues every kThreads/32-th row, in row order
+  {  // warp w stages every kThreads/32-th row, in row order; one elected lane issues the copies
+    // (the loop is warp-uniform, so the copy operands stay in uniform registers)
+    const int warp = __shfl_sync(0xFFFFFFFFu, tid >> 5, 0);
     const int P = (int)a.pitch;
-    for (int i = tid >> 5; i < nlist; i += kThreads / 32) {
+    const int base = x0 - K4;
+    const int lo = max(base, 0), hi = min(x0 + kW + K4, P);
+    const int lL = max(x0 - k, 0), hL = min(x0 - k + kW, P);
+    const int hC = min(x0 + kW, P);
+    const int lR = max(x0 + k, 0), hR = min(x0 + k + kW, P);
+    const uint32_t tx = spans3 ? 4u * (uint32_t)(max(hL - lL, 0) + (hC - x0) + max(hR - lR, 0)) : (uint32_t)(hi - lo) * 4u;
+    for (int i = warp; i < nlist; i += kThreads / 32) {
       int r = y0 + (i - 1) * k;       // outside the grid: stage the centre row again
       if (r < 0) r += k;
       else if (r >= N) r -= k;
       const uint32_t* src = BANDED ? row_ptr(a, r) : a.in + (int64_t)(r - a.row0) * a.pitch;
       uint32_t* dst = smem + (size_t)i * SE;
-      if (!spans3) {
-        const int base = x0 - K4;
-        const int lo = max(base, 0), hi = min(x0 + kW + K4, P);
-        mbar_expect_tx(&bars[i], (uint32_t)(hi - lo) * 4u);
-        bulk_g2s(dst + (lo - base), src + lo, (uint32_t)(hi - lo) * 4u, &bars[i]);
-      } else {
-        const int lL = max(x0 - k, 0), hL = min(x0 - k + kW, P);
-        const int lC = x0, hC = min(x0 + kW, P);
-        const int lR = max(x0 + k, 0), hR = min(x0 + k + kW, P);
-        mbar_expect_tx(&bars[i], 4u * (uint32_t)(max(hL - lL, 0) + (hC - lC) + max(hR - lR, 0)));
-        if (lL < hL) bulk_g2s(dst + (lL - (x0 - k)), src + lL, (uint32_t)(hL - lL) * 4u, &bars[i]);
-        bulk_g2s(dst + kW, src + lC, (uint32_t)(hC - lC) * 4u, &bars[i]);
-        if (lR < hR) bulk_g2s(dst + 2 * kW + (lR - (x0 + k)), src + lR, (uint32_t)(hR - lR) * 4u, &bars[i]);
+      if (elect_one()) {
+        mbar_expect_tx(&bars[i], tx);
+        if (!spans3) {
+          bulk_g2s(dst + (lo - base), src + lo, (uint32_t)(hi - lo) * 4u, &bars[i]);
+        } else {
+          if (lL < hL) bulk_g2s(dst + (lL - (x0 - k)), src + lL, (uint32_t)(hL - lL) * 4u, &bars[i]);
+          bulk_g2s(dst + kW, src + x0, (uint32_t)(hC - x0) * 4u, &bars[i]);
+          if (lR < hR) bulk_g2s(dst + 2 * kW + (lR - (x0 + k)), src + lR, (uint32_t)(hR - lR) * 4u, &bars[i]);
+        }
       }
+      __syncwarp();
     }
   }
 
@@ -465,9 +480,8 @@ template <int KM, bool MAY_EMPTY, bool BANDED, int METRIC = 0, bool VN = false, 
 __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLOCKS) jump_pass_fast(PassArgs a) {
   static_assert(!(MAY_EMPTY && REL), "the windowed path takes complete diagrams only");
   extern __shared__ __align__(128) uint32_t dyn_smem[];
-  const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
-  const int wk = (int)(blockIdx.x / (unsigned)a.xblocks);
-  const int res = wk / a.segs, seg = wk - res * a.segs;
+  // grid (xblocks, segs, residues): launched x-fastest, then the walk segments of one residue
+  const int xb = (int)blockIdx.x, seg = (int)blockIdx.y, res = (int)blockIdx.z;
   const int x0 = xb * kW;
   const int y0 = a.y_lo + res + seg * a.walk * a.k;
   if (res >= a.k || y0 >= a.y_hi) return;  // uniform over the CTA

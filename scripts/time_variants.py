@@ -41,9 +41,16 @@ jms, jn, jpx = d.pass_timing()
 print(json.dumps({"frame_ms": e0.elapsed_time(e1) / 20, "pass_ms": ms / n, "pass_GBps": 8 * px / n / (ms / n * 1e-3) / 1e9,
                   "jfa_frame_ms": j0.elapsed_time(j1) / 5, "jfa_pass_ms": jms / jn, "hash3": hex(h)}))
 '''
-libs = sorted(glob.glob("build/variants/*.so")) + ["paper_2209_00117_b200/libvd.so"]
-for lib in libs:
-    env = dict(os.environ, VD_LIB=os.path.abspath(lib))
+# Usage: time_variants.py                      every build/variants/*.so + the in-tree libvd.so
+#        time_variants.py VAR=v1,v2,...         the in-tree libvd.so under each value of env VAR
+runs = []
+if len(sys.argv) > 1 and "=" in sys.argv[1]:
+    var, vals = sys.argv[1].split("=", 1)
+    runs = [(f"{var}={v}", "paper_2209_00117_b200/libvd.so", {var: v}) for v in vals.split(",")]
+else:
+    runs = [(os.path.basename(l), l, {}) for l in sorted(glob.glob("build/variants/*.so")) + ["paper_2209_00117_b200/libvd.so"]]
+for name, lib, extra in runs:
+    env = dict(os.environ, VD_LIB=os.path.abspath(lib), **extra)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
     out = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
-    print(f"{os.path.basename(lib):45s} {out}", flush=True)
+    print(f"{name:45s} {out}", flush=True)
