@@ -354,7 +354,29 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     const int hC = min(x0 + kW, P);
     const int lR = max(x0 + k, 0), hR = min(x0 + k + kW, P);
     const uint32_t tx = spans3 ? 4u * (uint32_t)(max(hL - lL, 0) + (hC - x0) + max(hR - lR, 0)) : (uint32_t)(hi - lo) * 4u;
-    for (int i = warp; i < nlist; i += kThreads / 32) {
+    if (!BANDED && !spans3) {
+      // one band, whole rows: the warp's rows i = warp, warp + W, ... advance by constant
+      // strides (W = kThreads/32 rows of k grid rows each); a row outside the grid is the centre
+      // row again (k rows back or forward)
+      constexpr int W = kThreads / 32;
+      const int64_t kp = (int64_t)k * a.pitch;
+      int r = y0 + (warp - 1) * k;
+      const uint32_t* src = a.in + (int64_t)(r - a.row0) * a.pitch + lo;
+      uint32_t dst = smem_u32(smem + (size_t)warp * SE + (lo - base));
+      uint32_t bar = smem_u32(&bars[warp]);
+      const uint32_t bytes = (uint32_t)(hi - lo) * 4u;
+      for (int i = warp; i < nlist; i += W, r += W * k, src += W * kp, dst += W * SE * 4, bar += W * 8) {
+        const uint32_t* s = r < 0 ? src + kp : (r >= N ? src - kp : src);
+        if (elect_one()) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+              "l"(s), "r"(bytes), "r"(bar)
+              : "memory");
+        }
+        __syncwarp();
+      }
+    } else for (int i = warp; i < nlist; i += kThreads / 32) {
       int r = y0 + (i - 1) * k;       // outside the grid: stage the centre row again
       if (r < 0) r += k;
       else if (r >= N) r -= k;
