@@ -262,7 +262,8 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
     R.cy[i] = (int)cy;
     if constexpr (METRIC == 0) {
       const uint32_t D = c * sh16 + (uint32_t)xs16[i % kVec];  // (cx - (x+e)) << 16  (exact, |dx| < 2^15)
-      R.q[i] = (int)(cy * cy + (uint32_t)__mulhi((int)D, (int)D));  // cy^2 + dx^2
+      const int dx = (int)D >> 16;                                // cx - (x+e)
+      R.q[i] = (int)(cy * cy + (uint32_t)(dx * dx));              // cy^2 + dx^2
     } else {
       R.q[i] = (int)__sad((int)(c & 0xFFFFu), (REL ? xr : x) + (i % kVec), 0u);  // |cx - (x+e)|
     }
