@@ -249,6 +249,7 @@ def run_gpu(args):
     for f in range(W):
         dj.djfa_step(disp_dev[f], d)
     passes = dj.last_passes()
+    packed = dj.last_packed_passes()  # passes of the last warm-up frame on the packed-key kernel
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -287,6 +288,7 @@ def run_gpu(args):
     barrier()
     jms = max_over_ranks(j0.elapsed_time(j1))
     jpasses = jf.last_passes()
+    jpacked = jf.last_packed_passes()
     jfps = K / (jms / 1000.0)
     sim_vs_jfa = dj.similarity(jf)  # Eq. 5, same frame, dJFA vs JFA
 
@@ -367,11 +369,12 @@ def run_gpu(args):
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"{args.config}: {cdesc}, dJFA time steps", "N": N, "seeds": s, "d_max": d,
-                       "passes_per_frame": passes, "parallelism": f"rowband{world}", "halo": halo_mode[0],
+                       "passes_per_frame": passes, "packed_passes_per_frame": packed, "parallelism": f"rowband{world}", "halo": halo_mode[0],
                        "l2": (f"inputs larger than L2 (two {4 * N * N / 2**30:g}-GiB ping-pong label buffers vs 126 MB L2)"
                               if 8 * N * N > 126e6 else "inputs fit in L2, no flush: a parity config, not the headline")},
             "gpix_pass_per_s": gpps,
             "jfa": {"value": jfps, "unit": "frames/s", "ms_per_frame": jms / K, "passes_per_frame": jpasses,
+                    "packed_passes_per_frame": jpacked,
                     "gpix_pass_per_s": N * N * jpasses * K / (jms / 1000.0) / 1e9},
             "speedup_vs_jfa": jfps and fps / jfps,
             "similarity_vs_jfa_pct": sim_vs_jfa,

@@ -200,6 +200,15 @@ vd_status vd_band(vd_handle h, uint32_t* row0, uint32_t* rows);
 /* Number of jump passes in the last vd_jfa / vd_djfa_step. */
 vd_status vd_last_passes(vd_handle h, uint32_t* passes);
 
+/* How many passes of the last vd_jfa / vd_djfa_step ran the packed-key evaluation (a pass
+ * whose input labels all lie within Euclidean distance 63 of their pixels, with k <= 64:
+ * one 31-bit key (d2, dy, dx) per candidate, same result as the lexicographic key of Table 1 /
+ * P:112 with the (d2, label) tie-break).  The locality of each pass's input is decided on the
+ * device by the kernel that wrote it (remap, or the previous pass); this call synchronises
+ * the handle's stream to read those flags.  Tracked on single-band Euclidean handles only
+ * (0 otherwise, or with env VD_NO_PACK=1). */
+vd_status vd_last_packed_passes(vd_handle h, uint32_t* passes);
+
 /* Wait for all work enqueued on the handle's stream. */
 vd_status vd_synchronize(vd_handle h);
 

@@ -22,7 +22,7 @@ __all__ = [
     "VDError", "load_library", "library_path", "VoronoiDiagram", "EMPTY",
     "vd_config", "vd_halo_plan_t", "vd_create", "vd_destroy", "vd_jfa", "vd_move_seeds",
     "vd_djfa_step", "vd_stf", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
-    "vd_get_seeds", "vd_band", "vd_last_passes", "vd_synchronize", "vd_set_pass_timing",
+    "vd_get_seeds", "vd_band", "vd_last_passes", "vd_last_packed_passes", "vd_synchronize", "vd_set_pass_timing",
     "vd_pass_timing", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
     "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "vd_peer_export",
     "vd_peer_attach", "vd_peer_status", "vd_label_hash_async", "EXPORTED_SYMBOLS",
@@ -91,6 +91,7 @@ _SIGS = {
     "vd_get_seeds": (ctypes.c_int32, [H, P]),
     "vd_band": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "vd_last_passes": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32)]),
+    "vd_last_packed_passes": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32)]),
     "vd_synchronize": (ctypes.c_int32, [H]),
     "vd_set_pass_timing": (ctypes.c_int32, [H, ctypes.c_int]),
     "vd_pass_timing": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64),
@@ -307,6 +308,12 @@ def vd_last_passes(h) -> int:
     return v.value
 
 
+def vd_last_packed_passes(h) -> int:
+    v = ctypes.c_uint32()
+    _check(load_library().vd_last_packed_passes(h, ctypes.byref(v)), "vd_last_packed_passes", h)
+    return v.value
+
+
 def vd_synchronize(h) -> None:
     _check(load_library().vd_synchronize(h), "vd_synchronize", h)
 
@@ -437,6 +444,9 @@ class VoronoiDiagram:
 
     def last_passes(self) -> int:
         return vd_last_passes(self.h)
+
+    def last_packed_passes(self) -> int:
+        return vd_last_packed_passes(self.h)
 
     def synchronize(self):
         vd_synchronize(self.h)

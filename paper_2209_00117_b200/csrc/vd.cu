@@ -107,6 +107,8 @@ void halo_plan(uint32_t N, uint32_t world, uint32_t rank, uint32_t k, vd_halo_pl
   p.send_bot_row0 = B - h;
 }
 
+constexpr uint32_t kLocSlots = 64;  // locality flags per frame (>= passes + 1)
+
 struct Shard {
   uint32_t row0 = 0, rows = 0;
   uint32_t* buf[2] = {nullptr, nullptr};  // ping-pong diagrams, rows x pitch
@@ -147,6 +149,14 @@ struct vd_ctx {
   cudaEvent_t copy_done = nullptr;
   uint32_t* fwd = nullptr;        // [N*N] forward map (dJFA), allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
+  // Locality flags of one frame (packed-key pass, vd_kernels.cuh): loc[i] = 0 iff every label
+  // of the input of the frame's i-th tracked pass lies within kLocR of its pixel.
+  uint32_t* loc = nullptr;     // device u32[kLocSlots]
+  bool loc_on = false;         // a JFA / dJFA frame is tracking locality
+  bool loc_valid = false;      // loc[loc_idx] describes the current diagram
+  uint32_t loc_idx = 0;
+  std::vector<std::pair<int32_t, uint32_t>> loc_passes;  // per tracked pass: (loc slot of its input or -1, k)
+  std::vector<std::pair<int32_t, uint32_t>> loc_last;    // ... of the last frame
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -175,6 +185,24 @@ struct vd_ctx {
 };
 
 namespace {
+
+// Locality tracking for one JFA / dJFA frame on one band (packed-key passes, vd_kernels.cuh).
+// Env VD_NO_PACK=1 turns it off (A/B timing and tests of the exact kernel).
+bool loc_begin(vd_ctx* h) {
+  static const bool off = [] { const char* e = getenv("VD_NO_PACK"); return e && e[0] == '1'; }();
+  h->loc_on = !off && h->metric == 0 && h->world == 1 && h->shards.size() == 1;
+  h->loc_idx = 0;
+  h->loc_valid = false;
+  h->loc_passes.clear();
+  if (h->loc_on && cudaMemsetAsync(h->loc, 0, kLocSlots * sizeof(uint32_t), h->stream) != cudaSuccess)
+    h->loc_on = false;
+  return h->loc_on;
+}
+void loc_end(vd_ctx* h) {
+  h->loc_on = h->loc_valid = false;
+  h->loc_last.swap(h->loc_passes);
+  h->loc_passes.clear();
+}
 
 vd_status fail(vd_ctx* h, vd_status st, const char* fmt, ...) {
   char buf[512];
@@ -348,6 +376,8 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.metric = h->metric;
   a.vn = vn ? 1 : 0;
   a.empty_flag = h->track_empty ? h->counter : nullptr;
+  a.loc_in = nullptr;
+  a.loc_out = nullptr;
   if (y_lo < 0) { y_lo = (int64_t)sh.row0; y_hi = (int64_t)(sh.row0 + sh.rows); }
   a.y_lo = (int)y_lo;
   a.y_hi = (int)y_hi;
@@ -372,6 +402,16 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     while ((1u << a.lk) < k) ++a.lk;
     const dim3 grid((unsigned)a.xblocks, (unsigned)a.segs, nres), blk(vdk::kThreads);
     const bool banded = sh.top[0] != nullptr;
+    // locality tracking: Euclidean Moore passes on one band (the kernels' LOC variants)
+    const bool loc_track = h->loc_on && !banded && h->shards.size() == 1 && h->metric == 0 && !vn &&
+                           h->loc_idx + 1 < kLocSlots;
+    if (loc_track) {
+      a.loc_in = h->loc_valid ? h->loc + h->loc_idx : nullptr;
+      h->loc_passes.emplace_back(h->loc_valid ? (int32_t)h->loc_idx : -1, k);
+      a.loc_out = h->loc + h->loc_idx + 1;
+      ++h->loc_idx;
+    }
+    h->loc_valid = loc_track;
     const size_t sm = vdk::pass_smem((int)k, rel);
     cudaError_t e;
     if (k == 1) e = launch_fast_k<1>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
@@ -379,6 +419,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     else e = launch_fast_k<4>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     CK(e);
   } else {
+    h->loc_valid = false;  // the wide kernel does not report locality
     a.segs = 1;
     a.walk = 1;
     const int64_t blocks = (int64_t)a.xblocks * R;
@@ -589,6 +630,7 @@ void free_all(vd_ctx* h) {
   cudaFree(h->disp_buf[1]);
   cudaFree(h->fwd);
   cudaFree(h->counter);
+  cudaFree(h->loc);
 
   if (h->counter_h) cudaFreeHost(h->counter_h);
   for (auto e : h->disp_used)
@@ -815,6 +857,7 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
     CKC(cudaEventRecord(e, h->stream));
   }
   CKC(cudaMalloc(&h->counter, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->loc, kLocSlots * sizeof(uint32_t)));
   CKC(cudaMalloc(&h->flags, 2 * sizeof(uint32_t)));
   CKC(cudaMemset(h->flags, 0, 2 * sizeof(uint32_t)));
   CKC(cudaMalloc(&h->peer_err, sizeof(uint32_t)));
@@ -855,6 +898,7 @@ vd_status vd_jfa(vd_handle h) {
   // the remaining passes take the EMPTY-free kernels (a complete map stays complete).
   bool may_empty = !virt;
   const bool track = may_empty;
+  loc_begin(h);  // the passes report locality; once it holds, the rest take the packed-key kernel
   for (size_t i = 0; i < ks.size(); ++i) {
     const bool vn = i < h->jfa_vn_waves;
     if (track && may_empty) {
@@ -866,13 +910,14 @@ vd_status vd_jfa(vd_handle h) {
     const bool far = h->N > 32768 && ks[i] > 256;
     st = run_pass(h, ks[i], may_empty || far, vn, i + 1 < ks.size() ? ks[i + 1] : 0);
     h->track_empty = false;
-    if (st) return st;
+    if (st) return loc_end(h), st;
     if (track && may_empty) {
       uint64_t any = 1;
-      if ((st = reduce_to_host(h, &any))) return st;
+      if ((st = reduce_to_host(h, &any))) return loc_end(h), st;
       may_empty = any != 0;
     }
   }
+  loc_end(h);
   // A Moore JFA reaches every pixel (k_1 = 2^(ceil(log2 N)-1) covers every offset), so no V
   // survives; Von Neumann waves may leave some.
   h->last_passes = (uint32_t)ks.size();
@@ -953,10 +998,15 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   if ((st = after_launch(h, "move_fwd"))) return st;
   CK(cudaEventRecord(h->disp_used[slot], h->stream));
   // 2. labels follow their seeds (reuse of VD_{t-1})
+  //    (one band: the remap also reports whether every label is within kLocR of its pixel,
+  //    which lets the passes take the packed-key kernel)
+  const bool loc = loc_begin(h);
   for (auto& sh : h->shards) {
-    vdk::remap<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd);
+    vdk::remap<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd,
+                                                           (int)sh.row0, loc ? h->loc : nullptr);
     if ((st = after_launch(h, "remap"))) return st;
   }
+  h->loc_valid = loc;
   // 3. re-stamp the new seed pixels; fwd back to all-EMPTY
   for (size_t g = 0; g < h->shards.size(); ++g) {
     Shard& sh = h->shards[g];
@@ -968,7 +1018,8 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   // 4. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
   //    seed), so no EMPTY exists.
   for (size_t i = 0; i < ks.size(); ++i)
-    if ((st = run_pass(h, ks[i], false, i < h->vn_waves, i + 1 < ks.size() ? ks[i + 1] : 0))) return st;
+    if ((st = run_pass(h, ks[i], false, i < h->vn_waves, i + 1 < ks.size() ? ks[i + 1] : 0))) return loc_end(h), st;
+  loc_end(h);
   h->last_passes = (uint32_t)ks.size();
   return VD_OK;
 }
@@ -1219,6 +1270,20 @@ vd_status vd_band(vd_handle h, uint32_t* row0, uint32_t* rows) {
 vd_status vd_last_passes(vd_handle h, uint32_t* passes) {
   if (!h || !passes) return VD_ERR_ARG;
   *passes = h->last_passes;
+  return VD_OK;
+}
+
+vd_status vd_last_packed_passes(vd_handle h, uint32_t* passes) {
+  CHECK_HANDLE(h);
+  if (!passes) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  uint32_t flags[kLocSlots];
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(flags, h->loc, sizeof flags, cudaMemcpyDeviceToHost));
+  uint32_t n = 0;
+  for (const auto& p : h->loc_last)
+    if (p.first >= 0 && p.second <= (uint32_t)vdk::kPackMaxK && flags[p.first] == 0u) ++n;
+  *passes = n;
   return VD_OK;
 }
 

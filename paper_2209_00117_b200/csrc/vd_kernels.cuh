@@ -56,7 +56,18 @@ struct PassArgs {
   uint32_t* push_top;
   uint32_t* push_bot;
   int32_t push_k;
+  // Locality flags (packed-key pass, see walk): loc_in -> 0 iff every label of the INPUT lies
+  // within Euclidean distance kLocR of its own pixel (written by the previous kernel of the
+  // frame); null = unknown.  loc_out (or null): set to 1 if some OUTPUT label may lie farther.
+  const uint32_t* loc_in;
+  uint32_t* loc_out;
 };
+
+// Locality radius of the packed-key pass: with every input label within kLocR of its pixel
+// and k <= kPackMaxK, every candidate of every pixel has |dx|, |dy| <= kLocR + k <= 127.
+constexpr int kLocR = 63;
+constexpr int kPackMaxK = 64;
+constexpr uint32_t kLocD2 = (uint32_t)kLocR * kLocR;  // d2 bound of a "local" label
 
 // Store one output vector of row y (band-local pointer po) and, for the rows a neighbour's
 // next pass reads as halo, the same vector into its halo buffer.
@@ -278,7 +289,7 @@ __device__ __forceinline__ void row_from_smem(const uint32_t* __restrict__ st, i
 // term is c_i, for d_i > m the difference wraps to >= 2^31, above every label in use
 // (< 2^31).
 template <int METRIC, bool VN>
-__device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Row& Cn, int e, int y) {
+__device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Row& Cn, int e, int y, int& mo) {
   constexpr int n = VN ? 5 : 9;
   uint32_t c[9];
   int d[9];
@@ -302,12 +313,75 @@ __device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Ro
   int m;
   if constexpr (VN) m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), d[3], d[4]);
   else m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), __vimin3_s32(d[3], d[4], d[5]), __vimin3_s32(d[6], d[7], d[8]));
+  mo = m;
   uint32_t w[9];
 #pragma unroll
   for (int i = 0; i < n; ++i) w[i] = __viaddmax_u32((uint32_t)m, 0u - (uint32_t)d[i], c[i]);  // max(m - d_i, c_i)
   if constexpr (VN) return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), w[3], w[4]);
   else return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]),
                            __vimin3_u32(w[6], w[7], w[8]));
+}
+
+// ---- packed-key pass (labels local to their pixels: dJFA after the remap) -----------
+// When every candidate of a pixel (X, y) has |dx|, |dy| <= 127 (dx = cx - X, dy = cy - y),
+// the lexicographic key (d2, c) of R-3 -- for a fixed pixel the same order as (d2, dy, dx) --
+// fits ONE 31-bit integer:
+//   key = d2 * 2^16 + (dy + 128) * 2^8 + (dx + 128),   d2 <= 2 * 127^2 < 2^15,
+// so a single nine-way minimum (no tie-break pass) picks the winner, and its label is
+// recovered from the key's low bytes: ((y + dy) << 16) | (X + dx).  Per label (once per
+// staged row) Qk = (cy^2 + dx^2) * 2^16 + dx; per candidate ONE IMAD, Qk + cy * M_y with
+// M_y = 256 - 2y * 2^16, gives key - C_y (mod 2^32), C_y = y^2 2^16 - 256 y + 32896 common to
+// the pixel's candidates.  Those values lie in [-C_y, -C_y + 2^31) mod 2^32, an interval that
+// does not wrap as unsigned when -C_y <= 2^31 and as signed otherwise; the comparison kind is
+// chosen per output row (y is uniform over the CTA).
+template <int KM, bool FIX>
+__device__ __forceinline__ void row_packed(const uint32_t* __restrict__ st, int li, int ci, int ri, int x, int k, int N,
+                                           uint32_t sh16, const int (&xs16p)[kVec], Row& R) {
+  using V = typename VecT<kVec>::T;
+  uint32_t w[3 * kVec];
+  uint32_t c[3 * kVec];
+  unpack(*reinterpret_cast<const V*>(st + li), w);
+  unpack(*reinterpret_cast<const V*>(st + ci), w + kVec);
+  unpack(*reinterpret_cast<const V*>(st + ri), w + 2 * kVec);
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) {
+    if constexpr (KM >= kVec) { c[e] = w[e]; c[2 * kVec + e] = w[2 * kVec + e]; }
+    else { c[e] = w[kVec + e - KM]; c[2 * kVec + e] = w[kVec + e + KM]; }
+    c[kVec + e] = w[kVec + e];
+  }
+  if constexpr (FIX) {
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      if (x + e - k < 0) c[e] = w[kVec + e];
+      if (x + e + k >= N) c[2 * kVec + e] = w[kVec + e];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3 * kVec; ++i) {
+    const uint32_t cy = c[i] >> 16;
+    const uint32_t D1 = c[i] * sh16 + (uint32_t)xs16p[i % kVec];  // (cx - X) << 16 | 1
+    const uint32_t dx = (uint32_t)((int)D1 >> 16);
+    R.cy[i] = (int)cy;
+    R.q[i] = (int)(dx * D1 + cy * (c[i] & 0xFFFF0000u));  // (dx^2 + cy^2) << 16 + dx  (mod 2^32)
+  }
+}
+
+template <bool SIGNED>
+__device__ __forceinline__ uint32_t min9_packed(const Row& A, const Row& B, const Row& Cn, int e, uint32_t My) {
+  uint32_t kk[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    kk[j] = (uint32_t)A.q[kVec * j + e] + (uint32_t)A.cy[kVec * j + e] * My;
+    kk[3 + j] = (uint32_t)B.q[kVec * j + e] + (uint32_t)B.cy[kVec * j + e] * My;
+    kk[6 + j] = (uint32_t)Cn.q[kVec * j + e] + (uint32_t)Cn.cy[kVec * j + e] * My;
+  }
+  if constexpr (SIGNED)
+    return (uint32_t)__vimin3_s32(__vimin3_s32((int)kk[0], (int)kk[1], (int)kk[2]),
+                                  __vimin3_s32((int)kk[3], (int)kk[4], (int)kk[5]),
+                                  __vimin3_s32((int)kk[6], (int)kk[7], (int)kk[8]));
+  else
+    return __vimin3_u32(__vimin3_u32(kk[0], kk[1], kk[2]), __vimin3_u32(kk[3], kk[4], kk[5]),
+                        __vimin3_u32(kk[6], kk[7], kk[8]));
 }
 
 // Exact candidate test, key (distance, label) with EMPTY = +infinity, metric fixed at compile
@@ -329,7 +403,10 @@ __device__ __forceinline__ void consider64(uint32_t c, int x, int y, uint64_t& b
 // the centre row (the producer stages that row again), columns outside the grid by the
 // pixel's own column: duplicates never change a minimum.
 // BANDED: rows beyond the band come from the halo buffers (row_ptr).
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, int METRIC, bool VN, bool REL>
+// PACK: the packed-key evaluation (row_packed / min9_packed), taken when the input's locality
+// flag is clear and k <= kPackMaxK.  LOC variants (Euclidean Moore, one band) also report the
+// output's locality into a.loc_out.
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, int METRIC, bool VN, bool REL, bool PACK>
 __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t* smem) {
   const int k = a.k, N = a.N;
   const int tid = (int)threadIdx.x;
@@ -407,7 +484,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   // grid allows, so that a label outside the window always sets bit 15 of a 16-bit lane
   // after the subtraction.
   int ox = 0, oy = 0;
-  if constexpr (REL) {
+  if constexpr (REL && !PACK) {
     const int omax = max(N - 32768, 0);  // window kept inside the grid
     ox = min(max(x0 + kW / 2 - 16384, 0), omax);
     oy = min(max(y0 + ((nout - 1) * k) / 2 - 16384, 0), omax);
@@ -418,12 +495,20 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   int xs16[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) xs16[e] = -((x - ox + e) << 16);
+  int xs16p[kVec], xb[kVec];
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) { xs16p[e] = 1 - ((x + e) << 16); xb[e] = x + e - 128; }
   const bool active = x < N;
+  constexpr bool LOC = METRIC == 0 && !VN && !BANDED;
+  uint32_t loc_acc = 0;    // PACK: max true key of this thread's outputs
+  bool loc_bad = false;    // exact path: some output label farther than kLocR
 
   auto consume = [&](int i, Row& R) {
     mbar_wait(&bars[i], 0u);
-    row_from_smem<KM, MAY_EMPTY, FIX, METRIC, REL>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16,
-                                                   R, nbase2, &bad, x - ox);
+    if constexpr (PACK) row_packed<KM, FIX>(smem + (size_t)i * SE, li, ci, ri, x, k, N, sh16, xs16p, R);
+    else
+      row_from_smem<KM, MAY_EMPTY, FIX, METRIC, REL>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16,
+                                                     R, nbase2, &bad, x - ox);
   };
 
   Row r0, r1, r2;
@@ -438,12 +523,36 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   auto step = [&](const Row& P, const Row& C, Row& Nx) -> bool {
     consume(j + 2, Nx);
     uint32_t o[kVec];
+    if constexpr (PACK) {
+      const uint32_t uy = (uint32_t)y;
+      const uint32_t My = 256u - (uy << 17);
+      const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
+      const uint32_t Yb = (uy - 128u) << 16;
+      uint32_t sk[kVec];
+      if (0u - Cy <= 0x80000000u) {
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      uint32_t v = best_of<METRIC, VN>(P, C, Nx, e, y - oy);
-      if (MAY_EMPTY && !REL) v = (v == a.vempty) ? EMPTY : v;
-      if (REL) v = __vadd2(v, base2);  // back to absolute coordinates
-      o[e] = v;
+        for (int e = 0; e < kVec; ++e) sk[e] = min9_packed<false>(P, C, Nx, e, My) + Cy;
+      } else {
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) sk[e] = min9_packed<true>(P, C, Nx, e, My) + Cy;
+      }
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) o[e] = __byte_perm(sk[e], 0u, 0x4140) + Yb + (uint32_t)xb[e];
+      if constexpr (kVec == 4) loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
+      else loc_acc = __vimax3_u32(loc_acc, sk[0], sk[1]);
+    } else {
+      int mm = -0x7FFFFFFF - 1;
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) {
+        int me;
+        uint32_t v = best_of<METRIC, VN>(P, C, Nx, e, y - oy, me);
+        if constexpr (LOC) mm = max(mm, me);
+        if (MAY_EMPTY && !REL) v = (v == a.vempty) ? EMPTY : v;
+        if (REL) v = __vadd2(v, base2);  // back to absolute coordinates
+        o[e] = v;
+      }
+      // max d2 of the row's outputs = mm + (y - oy)^2 (m = d2 - y^2, see best_of)
+      if constexpr (LOC) loc_bad |= mm > (int)kLocD2 - (y - oy) * (y - oy);
     }
     if (active) {
       if constexpr (kVec == 4) store_out(a, BANDED, y, x, po, make_uint4(o[0], o[1], o[2], o[3]));
@@ -459,7 +568,16 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     if (!step(r1, r2, r0)) break;
     if (!step(r2, r0, r1)) break;
   }
-  if constexpr (REL) {
+  if constexpr (LOC) {
+    if (a.loc_out) {
+      bool far;
+      if constexpr (PACK) far = active && loc_acc >= ((kLocD2 + 1u) << 16);
+      else far = active && loc_bad;
+      if constexpr (REL && !PACK) far = far || (bad & 0x80008000u) != 0u;  // recomputed below: unknown
+      if (__syncthreads_or(far) && tid == 0) atomicOr(a.loc_out, 1u);
+    }
+  }
+  if constexpr (REL && !PACK) {
     // Some label of this walk lay outside the window: redo the walk exactly (64-bit keys)
     // from the staged rows, which are still in shared memory.  Never happens for a
     // converged dJFA diagram with dense seeds; keeps every grid exact.
@@ -514,8 +632,16 @@ __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLO
   // is exact as a centre-vector substitution.
   const int nstep = KM >= kVec ? a.k : kVec;
   const bool fix = (KM < kVec || (a.N & (kVec - 1))) && (x0 < nstep + kVec || x0 + kW + nstep + kVec > a.N);
-  if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN, REL>(a, x0, y0, dyn_smem);
-  else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN, REL>(a, x0, y0, dyn_smem);
+  constexpr bool CAN_PACK = METRIC == 0 && !VN && !BANDED && !MAY_EMPTY;
+  if constexpr (CAN_PACK) {
+    if (a.loc_in && a.k <= kPackMaxK && *(volatile const uint32_t*)a.loc_in == 0u) {
+      if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN, REL, true>(a, x0, y0, dyn_smem);
+      else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN, REL, true>(a, x0, y0, dyn_smem);
+      return;
+    }
+  }
+  if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN, REL, false>(a, x0, y0, dyn_smem);
+  else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN, REL, false>(a, x0, y0, dyn_smem);
 }
 
 // ------------------------------------------------------------------ wide jump pass
@@ -703,9 +829,12 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
 // Neighbouring pixels mostly share a label, so the gathers hit L1.
 // Row-major sweeps below: CTAs stride over rows, threads over 4-label quads of a row, with
 // the quad loop unrolled so that several 128-bit loads are in flight per thread.
-__global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd) {
+__global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd,
+                      int row0, uint32_t* __restrict__ loc) {
+  bool far = false;  // some remapped label farther than kLocR from its pixel (loc != null)
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     uint32_t* row = g + (int64_t)r * pitch;
+    const int y = row0 + r;
 #pragma unroll 4
     for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
       uint4* p = reinterpret_cast<uint4*>(row + x);
@@ -714,11 +843,21 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t c = w[e];
-        if (x + e < N && c != EMPTY) w[e] = __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu));
+        if (x + e < N) {
+          if (c != EMPTY) {
+            const uint32_t nc = __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu));
+            w[e] = nc;
+            const uint32_t dx = (nc & 0xFFFFu) - (uint32_t)(x + e), dy = (nc >> 16) - (uint32_t)y;
+            far |= dx + 63u > 126u || dy + 63u > 126u || dx * dx + dy * dy > kLocD2;  // (EMPTY is far)
+          } else {
+            far = true;
+          }
+        }
       }
       *p = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+  if (loc && __syncthreads_or(far) && threadIdx.x == 0) atomicOr(loc, 1u);
 }
 
 // ------------------------------------------------------------------ reductions

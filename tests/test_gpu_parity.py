@@ -564,3 +564,75 @@ def test_label_hash_async_matches(vd):
         want.append(oracle.label_hash(ref))
     d.synchronize()
     assert [int(v) & 0xFFFFFFFFFFFFFFFF for v in out] == want
+
+
+# ---- packed-key passes (labels local to their pixels; vd_kernels.cuh row_packed) ---------
+# The kernel switches to the one-key evaluation when the kernel that wrote its input found
+# every label within distance 63 of its pixel (and k <= 64).  The result must not change:
+# bit-exact against the same oracle, whichever path ran.
+
+
+def _djfa_frames_packed(vd, N, s, dmax, frames, seed, **cfg):
+    xy = synth.uniform_seeds(N, s, rng_seed=seed)
+    d = _jfa_gpu(vd, N, xy, **cfg)
+    G = oracle.jfa(N, xy)
+    assert np.array_equal(d.labels(), G)
+    packed = []
+    for f in range(frames):
+        disp = synth.displacements(s, dmax, f, rng_seed=seed)
+        d.djfa_step(disp, dmax)
+        G, xy, n = oracle.djfa_step(N, xy, disp, dmax, G)
+        packed.append(d.last_packed_passes())
+        assert np.array_equal(d.labels(), G), (f, packed)
+    return d, packed
+
+
+def test_packed_passes_taken_on_dense_seeds(vd):
+    # L_avg = 16 (the C3-C5 density): the remapped diagram is local, every delta pass
+    # (32 ... 1) takes the packed kernel
+    d, packed = _djfa_frames_packed(vd, 1024, 4096, 1, 4, 77)
+    assert packed == [d.last_passes()] * 4
+
+
+@pytest.mark.parametrize("s,dmax", [(16, 1), (64, 2), (128, 1), (256, 3), (512, 1), (2048, 5), (4096, 40)])
+def test_packed_passes_density_sweep_bit_exact(vd, s, dmax):
+    # From sparse (every remap far: exact kernel throughout) to dense (all packed), with
+    # densities in between where single frames or single passes switch paths.
+    d, packed = _djfa_frames_packed(vd, 512, s, dmax, 4, 1000 + s)
+    if s == 16:
+        assert packed == [0] * 4
+    if s >= 2048:
+        assert min(packed) > 0
+
+
+@pytest.mark.parametrize("N", [1000, 1031])
+def test_packed_passes_ragged_grid_bit_exact(vd, N):
+    # N not a multiple of 512 (edge CTAs) / of 4 (partial vectors)
+    d, packed = _djfa_frames_packed(vd, N, N * N // 256, 1, 3, N)
+    assert max(packed) > 0
+
+
+def test_packed_passes_disabled_env(vd, tmp_path):
+    # VD_NO_PACK=1 (read once per process): the exact kernel only, same labels
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, synth, oracle, paper_2209_00117_b200 as vd\n"
+        "N, s = 512, 1024\n"
+        "xy = synth.uniform_seeds(N, s, rng_seed=5)\n"
+        "d = vd.VoronoiDiagram(N, xy); d.jfa(); G = oracle.jfa(N, xy)\n"
+        "disp = synth.displacements(s, 1, 0, rng_seed=5)\n"
+        "d.djfa_step(disp, 1); G, xy, n = oracle.djfa_step(N, xy, disp, 1, G)\n"
+        "assert d.last_packed_passes() == 0\n"
+        "assert np.array_equal(d.labels(), G)\n"
+    )
+    env = dict(os.environ, VD_NO_PACK="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_packed_passes_windowed_kernel_forced(vd, monkeypatch):
+    # The windowed kernel (grids beyond 32768) carries the packed path too; forced at small N
+    monkeypatch.setenv("VD_FORCE_WINDOWED", "1")
+    d, packed = _djfa_frames_packed(vd, 1024, 4096, 2, 3, 91)
+    assert min(packed) > 0
