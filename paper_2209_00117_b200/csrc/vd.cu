@@ -157,6 +157,9 @@ struct vd_ctx {
   uint32_t loc_idx = 0;
   std::vector<std::pair<int32_t, uint32_t>> loc_passes;  // per tracked pass: (loc slot of its input or -1, k)
   std::vector<std::pair<int32_t, uint32_t>> loc_last;    // ... of the last frame
+  const uint32_t* pass_loc_in = nullptr;  // the running pass's input flag (null: unknown)
+  uint32_t* pass_loc_out = nullptr;       // ... and output flag (null: not tracked)
+  bool pass_loc_ok = false;               // every launch of the pass reported into pass_loc_out
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -190,13 +193,31 @@ namespace {
 // Env VD_NO_PACK=1 turns it off (A/B timing and tests of the exact kernel).
 bool loc_begin(vd_ctx* h) {
   static const bool off = [] { const char* e = getenv("VD_NO_PACK"); return e && e[0] == '1'; }();
-  h->loc_on = !off && h->metric == 0 && h->world == 1 && h->shards.size() == 1;
+  h->loc_on = !off && h->metric == 0;
   h->loc_idx = 0;
   h->loc_valid = false;
   h->loc_passes.clear();
   if (h->loc_on && cudaMemsetAsync(h->loc, 0, kLocSlots * sizeof(uint32_t), h->stream) != cudaSuccess)
     h->loc_on = false;
   return h->loc_on;
+}
+// One pass: its input flag is the previous pass's output flag; all of its launches (one per
+// shard, or interior + edge strips) OR into one output slot.
+void loc_pass_begin(vd_ctx* h, uint32_t k) {
+  h->pass_loc_in = nullptr;
+  h->pass_loc_out = nullptr;
+  h->pass_loc_ok = false;
+  if (!h->loc_on || h->loc_idx + 1 >= kLocSlots) return;
+  h->pass_loc_in = h->loc_valid ? h->loc + h->loc_idx : nullptr;
+  h->pass_loc_out = h->loc + h->loc_idx + 1;
+  h->pass_loc_ok = true;
+  h->loc_passes.emplace_back(h->loc_valid ? (int32_t)h->loc_idx : -1, k);
+}
+void loc_pass_end(vd_ctx* h) {
+  if (h->pass_loc_out) ++h->loc_idx;
+  h->loc_valid = h->pass_loc_out && h->pass_loc_ok;
+  h->pass_loc_in = nullptr;
+  h->pass_loc_out = nullptr;
 }
 void loc_end(vd_ctx* h) {
   h->loc_on = h->loc_valid = false;
@@ -402,16 +423,16 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     while ((1u << a.lk) < k) ++a.lk;
     const dim3 grid((unsigned)a.xblocks, (unsigned)a.segs, nres), blk(vdk::kThreads);
     const bool banded = sh.top[0] != nullptr;
-    // locality tracking: Euclidean Moore passes on one band (the kernels' LOC variants)
-    const bool loc_track = h->loc_on && !banded && h->shards.size() == 1 && h->metric == 0 && !vn &&
-                           h->loc_idx + 1 < kLocSlots;
-    if (loc_track) {
-      a.loc_in = h->loc_valid ? h->loc + h->loc_idx : nullptr;
-      h->loc_passes.emplace_back(h->loc_valid ? (int32_t)h->loc_idx : -1, k);
-      a.loc_out = h->loc + h->loc_idx + 1;
-      ++h->loc_idx;
+    // locality (the kernels' LOC variants: Euclidean Moore).  A launch whose rows read halo
+    // rows (written by other bands, whose locality this band's flag does not cover) keeps
+    // the exact walk; the interior launch of an overlapped sharded pass reads none.
+    if (h->pass_loc_out && h->metric == 0 && !vn) {
+      const bool reads_halo = banded && (a.y_lo < a.row0 + (int)k || a.y_hi > a.row0 + a.rows - (int)k);
+      a.loc_in = reads_halo ? nullptr : h->pass_loc_in;
+      a.loc_out = h->pass_loc_out;
+    } else {
+      h->pass_loc_ok = false;
     }
-    h->loc_valid = loc_track;
     const size_t sm = vdk::pass_smem((int)k, rel);
     cudaError_t e;
     if (k == 1) e = launch_fast_k<1>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
@@ -419,7 +440,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     else e = launch_fast_k<4>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     CK(e);
   } else {
-    h->loc_valid = false;  // the wide kernel does not report locality
+    h->pass_loc_ok = false;  // the wide kernel does not report locality
     a.segs = 1;
     a.walk = 1;
     const int64_t blocks = (int64_t)a.xblocks * R;
@@ -481,7 +502,14 @@ vd_status exchange_halos(vd_ctx* h, uint32_t k, cudaStream_t st) {
 // Peer halos (h->peer, NEXT-3): the edge strips also store the rows the neighbours' next pass
 // (step k_next) reads straight into their halo buffers, so that pass needs no exchange; across
 // processes a flag in the neighbour's memory announces them (peer_signal / peer_wait).
+vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t k_next);
 vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false, uint32_t k_next = 0) {
+  loc_pass_begin(h, k);
+  const vd_status st = run_pass_body(h, k, may_empty, vn, k_next);
+  loc_pass_end(h);
+  return st;
+}
+vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t k_next) {
   vd_status st;
   const bool sharded = h->world > 1 || h->vshards > 1;
   const uint32_t B = h->shards[0].rows;

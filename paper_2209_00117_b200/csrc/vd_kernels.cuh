@@ -499,7 +499,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
 #pragma unroll
   for (int e = 0; e < kVec; ++e) { xs16p[e] = 1 - ((x + e) << 16); xb[e] = x + e - 128; }
   const bool active = x < N;
-  constexpr bool LOC = METRIC == 0 && !VN && !BANDED;
+  constexpr bool LOC = METRIC == 0 && !VN;
   uint32_t loc_acc = 0;    // PACK: max true key of this thread's outputs
   bool loc_bad = false;    // exact path: some output label farther than kLocR
 
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLO
   // is exact as a centre-vector substitution.
   const int nstep = KM >= kVec ? a.k : kVec;
   const bool fix = (KM < kVec || (a.N & (kVec - 1))) && (x0 < nstep + kVec || x0 + kW + nstep + kVec > a.N);
-  constexpr bool CAN_PACK = METRIC == 0 && !VN && !BANDED && !MAY_EMPTY;
+  constexpr bool CAN_PACK = METRIC == 0 && !VN && !MAY_EMPTY;
   if constexpr (CAN_PACK) {
     if (a.loc_in && a.k <= kPackMaxK && *(volatile const uint32_t*)a.loc_in == 0u) {
       if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN, REL, true>(a, x0, y0, dyn_smem);
@@ -829,34 +829,36 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
 // Neighbouring pixels mostly share a label, so the gathers hit L1.
 // Row-major sweeps below: CTAs stride over rows, threads over 4-label quads of a row, with
 // the quad loop unrolled so that several 128-bit loads are in flight per thread.
+// loc (or null): set to 1 unless every remapped label lies within Chebyshev distance 44 of
+// its pixel (hence within Euclidean 63 = kLocR, 44 * sqrt(2) < 63): the packed-key passes'
+// precondition (walk).  Tracked as max over pixels of (cy - y + 44, cx - x + 44) in two
+// 16-bit lanes (a lane outside [0, 88] wraps high).
 __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd,
                       int row0, uint32_t* __restrict__ loc) {
-  bool far = false;  // some remapped label farther than kLocR from its pixel (loc != null)
+  uint32_t mx = 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     uint32_t* row = g + (int64_t)r * pitch;
-    const int y = row0 + r;
+    const uint32_t nb = __vsub2(0x002C002Cu, ((uint32_t)(row0 + r) << 16));  // (44 - y, 44) per lane
 #pragma unroll 4
     for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
       uint4* p = reinterpret_cast<uint4*>(row + x);
       uint4 v = *p;
       uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      const uint32_t nbx = __vsub2(nb, (uint32_t)x);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t c = w[e];
         if (x + e < N) {
-          if (c != EMPTY) {
-            const uint32_t nc = __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu));
-            w[e] = nc;
-            const uint32_t dx = (nc & 0xFFFFu) - (uint32_t)(x + e), dy = (nc >> 16) - (uint32_t)y;
-            far |= dx + 63u > 126u || dy + 63u > 126u || dx * dx + dy * dy > kLocD2;  // (EMPTY is far)
-          } else {
-            far = true;
-          }
+          const uint32_t nc = c != EMPTY ? __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu)) : EMPTY;
+          w[e] = nc;
+          // (cy - y + 44, cx - x - e + 44); EMPTY is far
+          mx = __vmaxu2(mx, nc == EMPTY ? 0xFFFFFFFFu : __vadd2(nc, __vsub2(nbx, (uint32_t)e)));
         }
       }
       *p = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+  const bool far = (mx >> 16) > 88u || (mx & 0xFFFFu) > 88u;
   if (loc && __syncthreads_or(far) && threadIdx.x == 0) atomicOr(loc, 1u);
 }
 

@@ -636,3 +636,13 @@ def test_packed_passes_windowed_kernel_forced(vd, monkeypatch):
     monkeypatch.setenv("VD_FORCE_WINDOWED", "1")
     d, packed = _djfa_frames_packed(vd, 1024, 4096, 2, 3, 91)
     assert min(packed) > 0
+
+
+@pytest.mark.parametrize("G,peer", [(2, False), (4, False), (4, True), (8, True)])
+def test_packed_passes_sharded_bit_exact(vd, G, peer):
+    # Row bands: the interior launch of an overlapped pass (rows that read no halo) takes the
+    # packed walk when the band's own flag is clear; edge strips and non-overlapped passes
+    # (2k >= band height) stay exact.  Identical to the oracle and to one band.
+    N, s, dmax = 1024, 4096, 2
+    d, packed = _djfa_frames_packed(vd, N, s, dmax, 3, 300 + G, virtual_shards=G, peer_halos=peer)
+    assert min(packed) > 0
