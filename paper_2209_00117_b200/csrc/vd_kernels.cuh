@@ -362,7 +362,12 @@ __device__ __forceinline__ void row_packed(const uint32_t* __restrict__ st, int 
     const uint32_t D1 = c[i] * sh16 + (uint32_t)xs16p[i % kVec];  // (cx - X) << 16 | 1
     const uint32_t dx = (uint32_t)((int)D1 >> 16);
     R.cy[i] = (int)cy;
-    R.q[i] = (int)(dx * D1 + cy * (c[i] & 0xFFFF0000u));  // (dx^2 + cy^2) << 16 + dx  (mod 2^32)
+#ifdef VD_CHI_IMAD
+    const uint32_t chi = cy * sh16;  // cy << 16 on the FMA pipe (experiment knob)
+#else
+    const uint32_t chi = c[i] & 0xFFFF0000u;  // cy << 16
+#endif
+    R.q[i] = (int)(dx * D1 + cy * chi);  // (dx^2 + cy^2) << 16 + dx  (mod 2^32)
   }
 }
 
