@@ -834,6 +834,10 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
 // Neighbouring pixels mostly share a label, so the gathers hit L1.
 // Row-major sweeps below: CTAs stride over rows, threads over 4-label quads of a row, with
 // the quad loop unrolled so that several 128-bit loads are in flight per thread.
+#ifndef VD_REMAP_UNROLL
+#define VD_REMAP_UNROLL 4
+#endif
+constexpr int kRemapUnroll = VD_REMAP_UNROLL;  // row quads in flight per remap thread
 // loc (or null): set to 1 unless every remapped label lies within Chebyshev distance 44 of
 // its pixel (hence within Euclidean 63 = kLocR, 44 * sqrt(2) < 63): the packed-key passes'
 // precondition (walk).  Tracked as max over pixels of (cy - y + 44, cx - x + 44) in two
@@ -844,7 +848,7 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     uint32_t* row = g + (int64_t)r * pitch;
     const uint32_t nb = __vsub2(0x002C002Cu, ((uint32_t)(row0 + r) << 16));  // (44 - y, 44) per lane
-#pragma unroll 4
+#pragma unroll kRemapUnroll
     for (int x = 4 * (int)threadIdx.x; x < N; x += 4 * (int)blockDim.x) {
       uint4* p = reinterpret_cast<uint4*>(row + x);
       uint4 v = *p;

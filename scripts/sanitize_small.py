@@ -12,6 +12,8 @@ cases = [
     (64, 16, {}), (1031, 200, {}), (1024, 1024, {}), (256, 100, {"virtual_shards": 4}),
     (300, 50, {"metric": "manhattan", "vn_waves": 2}), (128, 30, {"jfa_vn_waves": 99}),
     (1024, 1024, {"virtual_shards": 4, "peer_halos": True}), (512, 300, {"virtual_shards": 2, "peer_halos": True}),
+    # dense (L_avg = 16): the dJFA passes take the packed-key walk, one band and sharded
+    (1024, 4096, {}), (1024, 4096, {"virtual_shards": 4}), (1000, 3906, {}),
 ]
 for N, s, cfg in cases:
     xy = synth.uniform_seeds(N, s, rng_seed=1)
@@ -26,7 +28,7 @@ for N, s, cfg in cases:
     e.stf()
     e.set_labels(d.labels())
     e.jump_pass(3)
-    print(N, s, cfg, hex(d.label_hash()), d.match_count(d), flush=True)
+    print(N, s, cfg, hex(d.label_hash()), d.match_count(d), "packed", d.last_packed_passes(), flush=True)
     d.close()
     e.close()
 
