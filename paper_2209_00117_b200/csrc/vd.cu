@@ -160,6 +160,7 @@ struct vd_ctx {
   const uint32_t* pass_loc_in = nullptr;  // the running pass's input flag (null: unknown)
   uint32_t* pass_loc_out = nullptr;       // ... and output flag (null: not tracked)
   bool pass_loc_ok = false;               // every launch of the pass reported into pass_loc_out
+  bool pass_loc_used = false;             // some launch of the pass could take the packed walk
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -207,6 +208,7 @@ void loc_pass_begin(vd_ctx* h, uint32_t k) {
   h->pass_loc_in = nullptr;
   h->pass_loc_out = nullptr;
   h->pass_loc_ok = false;
+  h->pass_loc_used = false;
   if (!h->loc_on || h->loc_idx + 1 >= kLocSlots) return;
   h->pass_loc_in = h->loc_valid ? h->loc + h->loc_idx : nullptr;
   h->pass_loc_out = h->loc + h->loc_idx + 1;
@@ -214,6 +216,7 @@ void loc_pass_begin(vd_ctx* h, uint32_t k) {
   h->loc_passes.emplace_back(h->loc_valid ? (int32_t)h->loc_idx : -1, k);
 }
 void loc_pass_end(vd_ctx* h) {
+  if (h->pass_loc_out && !h->pass_loc_used) h->loc_passes.back().first = -1;  // no launch could pack
   if (h->pass_loc_out) ++h->loc_idx;
   h->loc_valid = h->pass_loc_out && h->pass_loc_ok;
   h->pass_loc_in = nullptr;
@@ -428,8 +431,9 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     // the exact walk; the interior launch of an overlapped sharded pass reads none.
     if (h->pass_loc_out && h->metric == 0 && !vn) {
       const bool reads_halo = banded && (a.y_lo < a.row0 + (int)k || a.y_hi > a.row0 + a.rows - (int)k);
-      a.loc_in = reads_halo ? nullptr : h->pass_loc_in;
+      a.loc_in = reads_halo || k > (uint32_t)vdk::kPackMaxK ? nullptr : h->pass_loc_in;
       a.loc_out = h->pass_loc_out;
+      h->pass_loc_used |= a.loc_in != nullptr;
     } else {
       h->pass_loc_ok = false;
     }

@@ -646,3 +646,11 @@ def test_packed_passes_sharded_bit_exact(vd, G, peer):
     N, s, dmax = 1024, 4096, 2
     d, packed = _djfa_frames_packed(vd, N, s, dmax, 3, 300 + G, virtual_shards=G, peer_halos=peer)
     assert min(packed) > 0
+
+
+def test_packed_passes_sharded_counts_only_overlapped_passes(vd):
+    # G = 8 bands of 32 rows: the k = 32 and 16 passes (2k >= B) read halos in every launch and
+    # stay exact; only k = 8 ... 1 can pack
+    d, packed = _djfa_frames_packed(vd, 256, 256, 1, 3, 8, virtual_shards=8)
+    assert d.last_passes() == 6
+    assert 0 < min(packed) and max(packed) <= 4
