@@ -205,8 +205,8 @@ vd_status vd_last_passes(vd_handle h, uint32_t* passes);
  * one 31-bit key (d2, dy, dx) per candidate, same result as the lexicographic key of Table 1 /
  * P:112 with the (d2, label) tie-break).  The locality of each pass's input is decided on the
  * device by the kernel that wrote it (remap, or the previous pass); this call synchronises
- * the handle's stream to read those flags.  Tracked on Euclidean handles (0 for Manhattan,
- * or with env VD_NO_PACK=1).  Sharded: a band's flag covers its own rows only, so there the
+ * the handle's stream to read those flags.  Tracked for Moore passes with either metric (not
+ * Von Neumann waves; 0 with env VD_NO_PACK=1).  Sharded: a band's flag covers its own rows only, so there the
  * count is of passes whose interior launch (rows that read no halo) ran packed; the edge
  * strips keep the exact evaluation. */
 vd_status vd_last_packed_passes(vd_handle h, uint32_t* passes);

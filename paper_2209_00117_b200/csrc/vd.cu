@@ -194,7 +194,7 @@ namespace {
 // Env VD_NO_PACK=1 turns it off (A/B timing and tests of the exact kernel).
 bool loc_begin(vd_ctx* h) {
   static const bool off = [] { const char* e = getenv("VD_NO_PACK"); return e && e[0] == '1'; }();
-  h->loc_on = !off && h->metric == 0;
+  h->loc_on = !off;
   h->loc_idx = 0;
   h->loc_valid = false;
   h->loc_passes.clear();
@@ -429,7 +429,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     // locality (the kernels' LOC variants: Euclidean Moore).  A launch whose rows read halo
     // rows (written by other bands, whose locality this band's flag does not cover) keeps
     // the exact walk; the interior launch of an overlapped sharded pass reads none.
-    if (h->pass_loc_out && h->metric == 0 && !vn) {
+    if (h->pass_loc_out && !vn) {
       const bool reads_halo = banded && (a.y_lo < a.row0 + (int)k || a.y_hi > a.row0 + a.rows - (int)k);
       a.loc_in = reads_halo || k > (uint32_t)vdk::kPackMaxK ? nullptr : h->pass_loc_in;
       a.loc_out = h->pass_loc_out;

@@ -334,7 +334,10 @@ __device__ __forceinline__ uint32_t best_of(const Row& A, const Row& B, const Ro
 // the pixel's candidates.  Those values lie in [-C_y, -C_y + 2^31) mod 2^32, an interval that
 // does not wrap as unsigned when -C_y <= 2^31 and as signed otherwise; the comparison kind is
 // chosen per output row (y is uniform over the CTA).
-template <int KM, bool FIX>
+// Manhattan (dJFAm), METRIC 1: key = d * 2^16 + (dy + 128) * 2^8 + (dx + 128) with
+// d = |dx| + |dy| <= 254.  Per label Qm = |dx| * 2^16 + dx + 256 cy, kept with chi = cy << 16;
+// per candidate ONE VABSDIFF, |chi - (y << 16)| + Qm = key - C'_y, C'_y = 32896 - 256 y.
+template <int KM, bool FIX, int METRIC = 0>
 __device__ __forceinline__ void row_packed(const uint32_t* __restrict__ st, int li, int ci, int ri, int x, int k, int N,
                                            uint32_t sh16, const int (&xs16p)[kVec], Row& R) {
   using V = typename VecT<kVec>::T;
@@ -356,6 +359,16 @@ __device__ __forceinline__ void row_packed(const uint32_t* __restrict__ st, int 
       if (x + e + k >= N) c[2 * kVec + e] = w[kVec + e];
     }
   }
+  if constexpr (METRIC == 1) {
+#pragma unroll
+    for (int i = 0; i < 3 * kVec; ++i) {
+      const uint32_t chi = c[i] & 0xFFFF0000u;                          // cy << 16
+      const uint32_t D = c[i] * sh16 + (uint32_t)(xs16p[i % kVec] - 1);  // (cx - X) << 16
+      const int dx = (int)D >> 16;
+      R.cy[i] = (int)chi;
+      R.q[i] = (int)(__sad((int)D, 0, (uint32_t)dx) + (chi >> 8));     // |dx| << 16 + dx + 256 cy
+    }
+  } else {
 #pragma unroll
   for (int i = 0; i < 3 * kVec; ++i) {
     const uint32_t cy = c[i] >> 16;
@@ -369,16 +382,21 @@ __device__ __forceinline__ void row_packed(const uint32_t* __restrict__ st, int 
 #endif
     R.q[i] = (int)(dx * D1 + cy * chi);  // (dx^2 + cy^2) << 16 + dx  (mod 2^32)
   }
+  }
 }
 
-template <bool SIGNED>
+template <bool SIGNED, int METRIC = 0>
 __device__ __forceinline__ uint32_t min9_packed(const Row& A, const Row& B, const Row& Cn, int e, uint32_t My) {
   uint32_t kk[9];
+  auto key = [&](const Row& R, int i) -> uint32_t {
+    if constexpr (METRIC == 1) return __usad((uint32_t)R.cy[i], My, (uint32_t)R.q[i]);  // My = y << 16
+    else return (uint32_t)R.q[i] + (uint32_t)R.cy[i] * My;
+  };
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    kk[j] = (uint32_t)A.q[kVec * j + e] + (uint32_t)A.cy[kVec * j + e] * My;
-    kk[3 + j] = (uint32_t)B.q[kVec * j + e] + (uint32_t)B.cy[kVec * j + e] * My;
-    kk[6 + j] = (uint32_t)Cn.q[kVec * j + e] + (uint32_t)Cn.cy[kVec * j + e] * My;
+    kk[j] = key(A, kVec * j + e);
+    kk[3 + j] = key(B, kVec * j + e);
+    kk[6 + j] = key(Cn, kVec * j + e);
   }
   if constexpr (SIGNED)
     return (uint32_t)__vimin3_s32(__vimin3_s32((int)kk[0], (int)kk[1], (int)kk[2]),
@@ -504,13 +522,13 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
 #pragma unroll
   for (int e = 0; e < kVec; ++e) { xs16p[e] = 1 - ((x + e) << 16); xb[e] = x + e - 128; }
   const bool active = x < N;
-  constexpr bool LOC = METRIC == 0 && !VN;
+  constexpr bool LOC = !VN;
   uint32_t loc_acc = 0;    // PACK: max true key of this thread's outputs
   bool loc_bad = false;    // exact path: some output label farther than kLocR
 
   auto consume = [&](int i, Row& R) {
     mbar_wait(&bars[i], 0u);
-    if constexpr (PACK) row_packed<KM, FIX>(smem + (size_t)i * SE, li, ci, ri, x, k, N, sh16, xs16p, R);
+    if constexpr (PACK) row_packed<KM, FIX, METRIC>(smem + (size_t)i * SE, li, ci, ri, x, k, N, sh16, xs16p, R);
     else
       row_from_smem<KM, MAY_EMPTY, FIX, METRIC, REL>(smem + (size_t)i * SE, li, ci, ri, x, k, N, a.vempty, sh16, xs16,
                                                      R, nbase2, &bad, x - ox);
@@ -530,16 +548,17 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
     uint32_t o[kVec];
     if constexpr (PACK) {
       const uint32_t uy = (uint32_t)y;
-      const uint32_t My = 256u - (uy << 17);
-      const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
+      // Euclidean: M_y, C_y of row_packed's note; Manhattan: y << 16 and C'_y
+      const uint32_t My = METRIC == 1 ? uy << 16 : 256u - (uy << 17);
+      const uint32_t Cy = METRIC == 1 ? 32896u - 256u * uy : uy * uy * 65536u - 256u * uy + 32896u;
       const uint32_t Yb = (uy - 128u) << 16;
       uint32_t sk[kVec];
       if (0u - Cy <= 0x80000000u) {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) sk[e] = min9_packed<false>(P, C, Nx, e, My) + Cy;
+        for (int e = 0; e < kVec; ++e) sk[e] = min9_packed<false, METRIC>(P, C, Nx, e, My) + Cy;
       } else {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) sk[e] = min9_packed<true>(P, C, Nx, e, My) + Cy;
+        for (int e = 0; e < kVec; ++e) sk[e] = min9_packed<true, METRIC>(P, C, Nx, e, My) + Cy;
       }
 #pragma unroll
       for (int e = 0; e < kVec; ++e) o[e] = __byte_perm(sk[e], 0u, 0x4140) + Yb + (uint32_t)xb[e];
@@ -557,7 +576,10 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
         o[e] = v;
       }
       // max d2 of the row's outputs = mm + (y - oy)^2 (m = d2 - y^2, see best_of)
-      if constexpr (LOC) loc_bad |= mm > (int)kLocD2 - (y - oy) * (y - oy);
+      if constexpr (LOC) {
+        if constexpr (METRIC == 1) loc_bad |= mm > kLocR;  // m = |dy| + |dx| (>= Chebyshev)
+        else loc_bad |= mm > (int)kLocD2 - (y - oy) * (y - oy);
+      }
     }
     if (active) {
       if constexpr (kVec == 4) store_out(a, BANDED, y, x, po, make_uint4(o[0], o[1], o[2], o[3]));
@@ -576,7 +598,7 @@ __device__ __forceinline__ void walk(const PassArgs& a, int x0, int y0, uint32_t
   if constexpr (LOC) {
     if (a.loc_out) {
       bool far;
-      if constexpr (PACK) far = active && loc_acc >= ((kLocD2 + 1u) << 16);
+      if constexpr (PACK) far = active && loc_acc >= (((METRIC == 1 ? (uint32_t)kLocR : kLocD2) + 1u) << 16);
       else far = active && loc_bad;
       if constexpr (REL && !PACK) far = far || (bad & 0x80008000u) != 0u;  // recomputed below: unknown
       if (__syncthreads_or(far) && tid == 0) atomicOr(a.loc_out, 1u);
@@ -637,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLO
   // is exact as a centre-vector substitution.
   const int nstep = KM >= kVec ? a.k : kVec;
   const bool fix = (KM < kVec || (a.N & (kVec - 1))) && (x0 < nstep + kVec || x0 + kW + nstep + kVec > a.N);
-  constexpr bool CAN_PACK = METRIC == 0 && !VN && !MAY_EMPTY;
+  constexpr bool CAN_PACK = !VN && !MAY_EMPTY;
   if constexpr (CAN_PACK) {
     if (a.loc_in && a.k <= kPackMaxK && *(volatile const uint32_t*)a.loc_in == 0u) {
       if (fix) walk<KM, MAY_EMPTY, BANDED, true, METRIC, VN, REL, true>(a, x0, y0, dyn_smem);

@@ -654,3 +654,22 @@ def test_packed_passes_sharded_counts_only_overlapped_passes(vd):
     d, packed = _djfa_frames_packed(vd, 256, 256, 1, 3, 8, virtual_shards=8)
     assert d.last_passes() == 6
     assert 0 < min(packed) and max(packed) <= 4
+
+
+@pytest.mark.parametrize("N,s,dmax,G", [(1024, 4096, 1, 1), (1000, 3906, 3, 1), (512, 1024, 2, 1), (1024, 4096, 2, 4)])
+def test_packed_passes_manhattan_bit_exact(vd, N, s, dmax, G):
+    # dJFAm: the packed key with d = |dx| + |dy| (one VABSDIFF per candidate)
+    xy = synth.uniform_seeds(N, s, rng_seed=N + s)
+    d = vd.VoronoiDiagram(N, xy, metric="manhattan", virtual_shards=G)
+    d.jfa()
+    G_ = oracle.jfa(N, xy, metric="manhattan")
+    assert np.array_equal(d.labels(), G_)
+    packed = []
+    for f in range(3):
+        disp = synth.displacements(s, dmax, f, rng_seed=N)
+        d.djfa_step(disp, dmax)
+        G_, xy, _ = oracle.djfa_step(N, xy, disp, dmax, G_, metric="manhattan")
+        packed.append(d.last_packed_passes())
+        assert np.array_equal(d.labels(), G_), (f, packed)
+    if s * 256 >= N * N:
+        assert min(packed) > 0

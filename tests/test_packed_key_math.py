@@ -89,3 +89,43 @@ def test_locality_radius_bounds_the_key():
     assert 63 + 64 == 127 and 2 * 127 ** 2 < 2 ** 15
     # remap's Chebyshev 44 implies Euclidean <= 63
     assert 2 * 44 ** 2 <= 63 ** 2
+
+
+def packed_label_manhattan(X, y, c):
+    """Manhattan (METRIC 1) form: per label chi = cy << 16, Qm = |dx| << 16 + dx + 256 cy; per
+    candidate |chi - (y << 16)| + Qm = key - C'_y with C'_y = 32896 - 256 y."""
+    c = [int(v) for v in c]
+    k = []
+    for v in c:
+        chi = v & 0xFFFF0000
+        D = (v * 65536 - (X << 16)) % 2**32
+        Ds = D - 2**32 if D >= 2**31 else D
+        dx = Ds >> 16
+        Qm = (abs(Ds) + dx + (chi >> 8)) % 2**32
+        k.append((abs(chi - ((y << 16) % 2**32)) + Qm) % 2**32)
+    Cy = (32896 - 256 * y) % 2**32
+    if (-Cy) % 2**32 <= 2**31:
+        m = min(k)
+    else:
+        m = min((v - 2**32 if v >= 2**31 else v) for v in k) % 2**32
+    s = (m + Cy) % 2**32
+    prmt = ((s >> 8) & 0xFF) << 16 | (s & 0xFF)
+    return (prmt + (((y - 128) << 16) % 2**32) + (X - 128)) % 2**32, s
+
+
+def test_manhattan_packed_key_matches_lexicographic_key():
+    rng = np.random.default_rng(173)
+    for _ in range(3000):
+        X, y = int(rng.integers(127, 65536 - 127)), int(rng.integers(127, 65536 - 128))
+        if rng.random() < 0.5:  # equidistant offsets (ties in d = |dx| + |dy|)
+            a, b = int(rng.integers(0, 64)), int(rng.integers(0, 64))
+            d = np.array([(a, b), (-a, b), (a, -b), (-a, -b), (b, a), (-b, a), (b, -a), (-b, -a), (a + b, 0)])
+        else:
+            d = rng.integers(-127, 128, size=(9, 2))
+        c = ((y + d[:, 1]) << 16) | (X + d[:, 0])
+        cx, cy = c & 0xFFFF, c >> 16
+        dist = np.abs(cx - X) + np.abs(cy - y)
+        want = int(c[np.lexsort((c, dist))[0]])
+        got, s = packed_label_manhattan(X, y, c)
+        assert got == want, (X, y, d.tolist())
+        assert s >> 16 == int(dist.min())
