@@ -10,7 +10,7 @@ import json, os, sys
 sys.path.insert(0, os.getcwd())
 import torch, synth
 import paper_2209_00117_b200 as vd
-N, s = {"C4": (16384, 1 << 20), "C3": (4096, 65536)}[os.environ.get("VD_CFG", "C4")]
+N, s = {"C4": (16384, 1 << 20), "C3": (4096, 65536), "C5": (65536, 1 << 24)}[os.environ.get("VD_CFG", "C4")]
 xy = synth.uniform_seeds(N, s, rng_seed=2209)
 st = torch.cuda.Stream()
 d = vd.VoronoiDiagram(N, xy, device=0, stream=st.cuda_stream)
