@@ -30,8 +30,10 @@ __all__ = [
 
 EMPTY = 0xFFFFFFFF
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# VD_LIB overrides the library path (kernel-variant experiments in scripts/); default in-tree.
-_LIB_PATH = os.environ.get("VD_LIB") or os.path.join(_PKG, "libvd.so")
+# Always the in-tree build.  Kernel-variant experiments (scripts/time_variants.py) load
+# another build explicitly with _load_variant(path); no environment variable redirects the
+# product binding.
+_LIB_PATH = os.path.join(_PKG, "libvd.so")
 _lib = None
 
 VD_OK, VD_ERR_ARG, VD_ERR_RANGE, VD_ERR_STATE, VD_ERR_CUDA, VD_ERR_NCCL, VD_ERR_OOM = 0, -1, -2, -3, -4, -5, -6
@@ -122,13 +124,25 @@ def library_path() -> str:
 def load_library():
     """Load libvd.so (built by paper_2209_00117_b200.build / __graft_entry__.build()).
     Raises if it is missing: there is no fallback implementation."""
+    return _load(_LIB_PATH)
+
+
+def _load_variant(path: str):
+    """Experiments only (scripts/time_variants.py): bind a variant build of libvd instead of
+    the in-tree one.  Must be called before anything else loads the library."""
+    if _lib is not None:
+        raise RuntimeError("libvd is already loaded")
+    return _load(os.path.abspath(path))
+
+
+def _load(path: str):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_LIB_PATH):
-        raise RuntimeError(f"libvd.so not found at {_LIB_PATH}: run `python -m paper_2209_00117_b200.build` "
+    if not os.path.exists(path):
+        raise RuntimeError(f"libvd.so not found at {path}: run `python -m paper_2209_00117_b200.build` "
                            "(or __graft_entry__.build()); there is no CPU fallback")
-    lib = ctypes.CDLL(_LIB_PATH)
+    lib = ctypes.CDLL(path)
     for name, (res, args) in _SIGS.items():
         f = getattr(lib, name)
         f.restype = res

@@ -21,7 +21,9 @@ def _nccl_include() -> str:
 def nvcc_cmd(out: str = LIB, extra: list[str] | None = None) -> list[str]:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     return [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-            "-cudart", "static",
+            # shared cudart: in a torch process the already-loaded libcudart.so.12 is reused; the
+            # rpath finds the toolkit's copy when libvd is loaded on its own
+            "-cudart", "shared", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
             "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
             "-o", out, *SRC, "-ldl", *(extra or [])]
 

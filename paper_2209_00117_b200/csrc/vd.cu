@@ -11,6 +11,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -36,6 +39,8 @@ struct Nccl {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 Nccl g_nccl;
 
@@ -57,6 +62,8 @@ bool nccl_load() {
   VD_SYM(Recv, "ncclRecv");
   VD_SYM(AllReduce, "ncclAllReduce");
   VD_SYM(GetErrorString, "ncclGetErrorString");
+  VD_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+  VD_SYM(CommAbort, "ncclCommAbort");
 #undef VD_SYM
   g_nccl.ok = true;
   return true;
@@ -180,7 +187,8 @@ struct vd_ctx {
   uint32_t pushed_k = 0;       // the previous pass pushed this step's halos (0: none)
   uint32_t pass_seq = 0;       // passes run (same on every rank): signal sequence numbers
   uint32_t* flags = nullptr;   // device u32[2]: seq published by the band above / below
-  uint32_t* peer_err = nullptr;// device u32: a peer wait timed out
+  uint32_t* peer_err = nullptr;// device view of peer_err_h
+  uint32_t* peer_err_h = nullptr;  // mapped pinned host u32: a peer wait timed out (checked by every call)
   uint32_t* nbr_bot[2] = {nullptr, nullptr};  // band above's bottom halos (peer pointers)
   uint32_t* nbr_top[2] = {nullptr, nullptr};  // band below's top halos
   uint32_t* nbr_flag_above = nullptr;         // band above's flags[1]
@@ -254,18 +262,28 @@ vd_status fail(vd_ctx* h, vd_status st, const char* fmt, ...) {
     if (r_ != ncclSuccess) return fail(h, VD_ERR_NCCL, "%s: %s", #expr, g_nccl.GetErrorString(r_)); \
   } while (0)
 
-#define CHECK_HANDLE(h)                        \
-  do {                                         \
-    if (!(h)) return VD_ERR_ARG;               \
-    if ((h)->sticky != VD_OK) return (h)->sticky; \
+// A peer-halo wait that timed out on the device (vdk::peer_wait) wrote 1 into mapped host
+// memory: the halos of that pass were never received, so the diagram is wrong.  Every
+// entry point turns it into a sticky error before doing anything else.
+vd_status check_async(vd_ctx* h) {
+  if (h->sticky != VD_OK) return h->sticky;
+  if (h->peer_err_h && *(volatile uint32_t*)h->peer_err_h)
+    return fail(h, VD_ERR_CUDA, "a peer-halo wait timed out on the device (neighbour never signalled)");
+  return VD_OK;
+}
+
+#define CHECK_HANDLE(h)                                \
+  do {                                                 \
+    if (!(h)) return VD_ERR_ARG;                       \
+    if (vd_status s_ = check_async(h)) return s_;      \
   } while (0)
 
 // Row-sweep kernels (remap, match_count, label_hash, count_value): CTAs stride over rows.
-int rows_grid(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(rows, 148 * 8)); }
+int rows_grid(const vd_ctx* h, int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)h->num_sms * 8)); }
 
-int grid_for(int64_t work, int threads) {
+int grid_for(const vd_ctx* h, int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->num_sms * 32));
 }
 
 vd_status after_launch(vd_ctx* h, const char* what) {
@@ -273,6 +291,41 @@ vd_status after_launch(vd_ctx* h, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, VD_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
   return VD_OK;
+}
+
+// Wait for the handle's stream.  With an NCCL communicator, poll instead of blocking, so
+// that a failed or stuck collective (a dead peer) becomes VD_ERR_NCCL rather than a hang:
+// ncclCommGetAsyncError is checked while the stream is busy, and after VD_NCCL_TIMEOUT_S
+// seconds (default 600) the communicator is aborted.
+vd_status sync_stream(vd_ctx* h) {
+  if (!h->comm) {
+    CK(cudaStreamSynchronize(h->stream));
+    return check_async(h);
+  }
+  static const double limit = [] {
+    const char* e = getenv("VD_NCCL_TIMEOUT_S");
+    return e ? atof(e) : 600.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  while (true) {
+    const cudaError_t q = cudaStreamQuery(h->stream);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return fail(h, VD_ERR_CUDA, "stream: %s", cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    if (g_nccl.CommGetAsyncError(h->comm, &ar) != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+      g_nccl.CommAbort(h->comm);
+      h->comm = nullptr;
+      return fail(h, VD_ERR_NCCL, "NCCL asynchronous error: %s", g_nccl.GetErrorString(ar));
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      g_nccl.CommAbort(h->comm);
+      h->comm = nullptr;
+      return fail(h, VD_ERR_NCCL, "NCCL: stream did not finish within %.0f s (VD_NCCL_TIMEOUT_S); communicator aborted",
+                  limit);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  return check_async(h);
 }
 
 bool is_device_ptr(const void* p) {
@@ -327,33 +380,42 @@ vd_status timed_end(vd_ctx* h, uint64_t px) {
 
 // Which kernel variant can take this pass exactly (see vd_kernels.cuh).
 // Launch one fast-pass instantiation; each opts into the largest staging size once.
+// The dynamic shared-memory opt-in is a per-device function attribute: set it once per
+// (instantiation, device), remembered in a per-instantiation device bitmask (a concurrent
+// first use on two threads sets the same value twice, which is harmless).
 template <int KM, bool ME, bool BD, int MT, bool VN, bool REL>
-cudaError_t launch_fast(const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
-  static cudaError_t attr = cudaErrorNotReady;
-  if (attr == cudaErrorNotReady)
-    attr = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                REL ? vdk::kSmemBudgetRel : vdk::kSmemBudget);
-  if (attr != cudaSuccess) return attr;
+cudaError_t launch_fast(int dev, const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
+  static std::atomic<uint64_t> opted{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(opted.load(std::memory_order_acquire) & bit)) {
+    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               REL ? vdk::kSmemBudgetRel : vdk::kSmemBudget);
+    if (e != cudaSuccess) return e;
+    opted.fetch_or(bit, std::memory_order_release);
+  }
   vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL><<<grid, blk, sm, st>>>(a);
   return cudaSuccess;
 }
 template <int KM, bool ME, bool BD, bool REL>
-cudaError_t launch_fast_mv(int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
+cudaError_t launch_fast_mv(int dev, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm,
+                           cudaStream_t st) {
   if (metric == 0)
-    return vn ? launch_fast<KM, ME, BD, 0, true, REL>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 0, false, REL>(a, g, b, sm, st);
-  return vn ? launch_fast<KM, ME, BD, 1, true, REL>(a, g, b, sm, st) : launch_fast<KM, ME, BD, 1, false, REL>(a, g, b, sm, st);
+    return vn ? launch_fast<KM, ME, BD, 0, true, REL>(dev, a, g, b, sm, st)
+              : launch_fast<KM, ME, BD, 0, false, REL>(dev, a, g, b, sm, st);
+  return vn ? launch_fast<KM, ME, BD, 1, true, REL>(dev, a, g, b, sm, st)
+            : launch_fast<KM, ME, BD, 1, false, REL>(dev, a, g, b, sm, st);
 }
 template <int KM>
-cudaError_t launch_fast_k(bool me, bool bd, bool rel, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b,
-                          size_t sm, cudaStream_t st) {
+cudaError_t launch_fast_k(int dev, bool me, bool bd, bool rel, int metric, bool vn, const vdk::PassArgs& a, dim3 g,
+                          dim3 b, size_t sm, cudaStream_t st) {
   if (rel)  // windowed coordinates (complete diagrams beyond the plain fast kernel's range)
-    return bd ? launch_fast_mv<KM, false, true, true>(metric, vn, a, g, b, sm, st)
-              : launch_fast_mv<KM, false, false, true>(metric, vn, a, g, b, sm, st);
-  if (me) return bd ? launch_fast_mv<KM, true, true, false>(metric, vn, a, g, b, sm, st)
-                    : launch_fast_mv<KM, true, false, false>(metric, vn, a, g, b, sm, st);
-  return bd ? launch_fast_mv<KM, false, true, false>(metric, vn, a, g, b, sm, st)
-            : launch_fast_mv<KM, false, false, false>(metric, vn, a, g, b, sm, st);
+    return bd ? launch_fast_mv<KM, false, true, true>(dev, metric, vn, a, g, b, sm, st)
+              : launch_fast_mv<KM, false, false, true>(dev, metric, vn, a, g, b, sm, st);
+  if (me) return bd ? launch_fast_mv<KM, true, true, false>(dev, metric, vn, a, g, b, sm, st)
+                    : launch_fast_mv<KM, true, false, false>(dev, metric, vn, a, g, b, sm, st);
+  return bd ? launch_fast_mv<KM, false, true, false>(dev, metric, vn, a, g, b, sm, st)
+            : launch_fast_mv<KM, false, false, false>(dev, metric, vn, a, g, b, sm, st);
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
@@ -439,9 +501,9 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     }
     const size_t sm = vdk::pass_smem((int)k, rel);
     cudaError_t e;
-    if (k == 1) e = launch_fast_k<1>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
-    else if (k == 2) e = launch_fast_k<2>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
-    else e = launch_fast_k<4>(may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    if (k == 1) e = launch_fast_k<1>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    else if (k == 2) e = launch_fast_k<2>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    else e = launch_fast_k<4>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     CK(e);
   } else {
     h->pass_loc_ok = false;  // the wide kernel does not report locality
@@ -544,7 +606,7 @@ vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t
     if (multi_peer) {  // copy the edge rows into the neighbours' halos, then announce them
       const Shard& sh = h->shards[0];
       const int64_t n4 = (int64_t)k * (h->pitch / 4);
-      vdk::push_rows<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 8), 256, 0, h->halo_stream>>>(
+      vdk::push_rows<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, (int64_t)h->num_sms * 8), 256, 0, h->halo_stream>>>(
           sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, (int)k, has_above ? h->nbr_bot[h->hpar] : nullptr,
           has_below ? h->nbr_top[h->hpar] : nullptr);
       if ((st = after_launch(h, "push_rows"))) return st;
@@ -599,7 +661,7 @@ vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t
 
 vd_status stamp_all(vd_ctx* h, const uint32_t* seeds) {
   for (auto& sh : h->shards) {
-    vdk::stamp<<<grid_for((int64_t)h->s, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
+    vdk::stamp<<<grid_for(h, (int64_t)h->s, 256), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
                                                                    (int)sh.rows, seeds, (int64_t)h->s);
     vd_status st = after_launch(h, "stamp");
     if (st) return st;
@@ -612,7 +674,7 @@ vd_status move_seeds(vd_ctx* h, const int16_t* disp_xy) {
   int slot;
   vd_status st = upload_disp(h, disp_xy, &d, &slot);
   if (st) return st;
-  vdk::move_clamp<<<grid_for((int64_t)h->s, 256), 256, 0, h->stream>>>(h->seeds, d, h->seeds_new, (int64_t)h->s,
+  vdk::move_clamp<<<grid_for(h, (int64_t)h->s, 256), 256, 0, h->stream>>>(h->seeds, d, h->seeds_new, (int64_t)h->s,
                                                                        (int)h->N);
   if ((st = after_launch(h, "move_clamp"))) return st;
   CK(cudaEventRecord(h->disp_used[slot], h->stream));
@@ -625,7 +687,7 @@ vd_status reduce_to_host(vd_ctx* h, uint64_t* out) {
     CKN(g_nccl.AllReduce(h->counter, h->counter, 1, ncclUint64, ncclSum, h->comm, h->stream));
   }
   CK(cudaMemcpyAsync(h->counter_h, h->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st = sync_stream(h)) return st;
   *out = *h->counter_h;
   return VD_OK;
 }
@@ -654,7 +716,7 @@ void free_all(vd_ctx* h) {
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   h->ipc_opened.clear();
   cudaFree(h->flags);
-  cudaFree(h->peer_err);
+  if (h->peer_err_h) cudaFreeHost(h->peer_err_h);
   h->shards.clear();
   cudaFree(h->seeds);
   cudaFree(h->seeds_new);
@@ -694,7 +756,7 @@ vd_status jfa_init(vd_ctx* h) {
   const uint32_t u = unclaimed_label(h);
   for (auto& sh : h->shards) {
     const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
-    vdk::fill_value<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u);
+    vdk::fill_value<<<grid_for(h, n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u);
     vd_status st = after_launch(h, "fill_value");
     if (st) return st;
   }
@@ -707,7 +769,7 @@ vd_status jfa_finish(vd_ctx* h) {
   if (u == VD_EMPTY) return VD_OK;
   for (auto& sh : h->shards) {
     const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
-    vdk::replace_value<<<grid_for(n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u,
+    vdk::replace_value<<<grid_for(h, n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u,
                                                                  VD_EMPTY);
     vd_status st = after_launch(h, "replace_value");
     if (st) return st;
@@ -892,8 +954,9 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   CKC(cudaMalloc(&h->loc, kLocSlots * sizeof(uint32_t)));
   CKC(cudaMalloc(&h->flags, 2 * sizeof(uint32_t)));
   CKC(cudaMemset(h->flags, 0, 2 * sizeof(uint32_t)));
-  CKC(cudaMalloc(&h->peer_err, sizeof(uint32_t)));
-  CKC(cudaMemset(h->peer_err, 0, sizeof(uint32_t)));
+  CKC(cudaHostAlloc(&h->peer_err_h, sizeof(uint32_t), cudaHostAllocMapped));
+  *h->peer_err_h = 0;
+  CKC(cudaHostGetDevicePointer(&h->peer_err, h->peer_err_h, 0));
   h->peer = cfg.peer_halos && cfg.world == 1 && h->vshards > 1;  // across processes: vd_peer_attach
   CKC(cudaMallocHost(&h->counter_h, sizeof(unsigned long long)));
   CKC(cudaMemcpyAsync(h->seeds, packed.data(), s * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
@@ -958,7 +1021,7 @@ vd_status vd_jfa(vd_handle h) {
     // dJFA needs a complete diagram: count what is still EMPTY (synchronises)
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
     for (auto& sh : h->shards) {
-      vdk::count_value<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+      vdk::count_value<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
                                                                   VD_EMPTY, h->counter);
       if ((st = after_launch(h, "count_value"))) return st;
     }
@@ -982,7 +1045,7 @@ vd_status vd_stf(vd_handle h, uint32_t* passes) {
   while (true) {  // "until the grid is fully flooded": stop once no EMPTY is left
     CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
     for (auto& sh : h->shards) {
-      vdk::count_value<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+      vdk::count_value<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
                                                                   u, h->counter);
       if ((st = after_launch(h, "count_value"))) return st;
     }
@@ -1024,7 +1087,7 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   int slot;
   vd_status st = upload_disp(h, disp_xy, &dd, &slot);
   if (st) return st;
-  const int gs = grid_for((int64_t)h->s, 256);
+  const int gs = grid_for(h, (int64_t)h->s, 256);
   // 1. SimulateParticles + forward map old -> new (R-9); fwd is all EMPTY on entry
   vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N);
   if ((st = after_launch(h, "move_fwd"))) return st;
@@ -1034,7 +1097,7 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   //    which lets the passes take the packed-key kernel)
   const bool loc = loc_begin(h);
   for (auto& sh : h->shards) {
-    vdk::remap<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd,
+    vdk::remap<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd,
                                                            (int)sh.row0, loc ? h->loc : nullptr);
     if ((st = after_launch(h, "remap"))) return st;
   }
@@ -1075,7 +1138,7 @@ vd_status vd_set_labels(vd_handle h, const uint32_t* labels) {
                          h->N * sizeof(uint32_t), h->N * sizeof(uint32_t), sh.rows, cudaMemcpyHostToDevice, h->stream));
     off_rows += sh.rows;
   }
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st_ = sync_stream(h)) return st_;
   h->has_diagram = !any_empty;
   return VD_OK;
 }
@@ -1164,11 +1227,10 @@ vd_status vd_peer_attach(vd_handle h, const void* blobs, size_t len_each) {
 }
 
 vd_status vd_peer_status(vd_handle h, uint32_t* timed_out) {
-  CHECK_HANDLE(h);
-  if (!timed_out) return VD_ERR_ARG;
+  if (!h || !timed_out) return VD_ERR_ARG;
   DeviceGuard guard(h->device);
   CK(cudaStreamSynchronize(h->stream));
-  CK(cudaMemcpy(timed_out, h->peer_err, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  *timed_out = *(volatile uint32_t*)h->peer_err_h;
   return VD_OK;
 }
 
@@ -1185,7 +1247,7 @@ vd_status vd_similarity(vd_handle h, vd_handle ref, double* pct, uint64_t* match
   for (size_t g = 0; g < h->shards.size(); ++g) {
     const Shard& a = h->shards[g];
     const Shard& b = ref->shards[g];
-    vdk::match_count<<<rows_grid(a.rows), 256, 0, h->stream>>>(a.buf[h->cur], b.buf[ref->cur], h->pitch,
+    vdk::match_count<<<rows_grid(h, a.rows), 256, 0, h->stream>>>(a.buf[h->cur], b.buf[ref->cur], h->pitch,
                                                                 (int)a.rows, (int)h->N, h->counter);
     vd_status st = after_launch(h, "match_count");
     if (st) return st;
@@ -1209,7 +1271,7 @@ vd_status vd_similarity_host(vd_handle h, const uint32_t* ref_labels, double* pc
     uint32_t* scratch = sh.buf[h->cur ^ 1];
     CK(cudaMemcpy2DAsync(scratch, h->pitch * sizeof(uint32_t), ref_labels + off_rows * h->N, h->N * sizeof(uint32_t),
                          h->N * sizeof(uint32_t), sh.rows, cudaMemcpyDefault, h->stream));
-    vdk::match_count<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], scratch, h->pitch, (int)sh.rows,
+    vdk::match_count<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], scratch, h->pitch, (int)sh.rows,
                                                                 (int)h->N, h->counter);
     vd_status st = after_launch(h, "match_count");
     if (st) return st;
@@ -1227,7 +1289,7 @@ namespace {
 vd_status enqueue_label_hash(vd_ctx* h) {
   CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
   for (auto& sh : h->shards) {
-    vdk::label_hash<<<rows_grid(sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
+    vdk::label_hash<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0,
                                                                (int)sh.rows, (int)h->N, h->counter);
     vd_status st = after_launch(h, "label_hash");
     if (st) return st;
@@ -1269,7 +1331,7 @@ vd_status vd_get_labels(vd_handle h, uint32_t* out) {
                          h->N * sizeof(uint32_t), sh.rows, cudaMemcpyDeviceToHost, h->stream));
     off_rows += sh.rows;
   }
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st_ = sync_stream(h)) return st_;
   return VD_OK;
 }
 
@@ -1279,7 +1341,7 @@ vd_status vd_get_seeds(vd_handle h, uint16_t* out_xy) {
   DeviceGuard guard(h->device);
   std::vector<uint32_t> p(h->s);
   CK(cudaMemcpyAsync(p.data(), h->seeds, h->s * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st_ = sync_stream(h)) return st_;
   for (uint64_t i = 0; i < h->s; ++i) {
     out_xy[2 * i] = (uint16_t)(p[i] & 0xFFFFu);
     out_xy[2 * i + 1] = (uint16_t)(p[i] >> 16);
@@ -1310,7 +1372,7 @@ vd_status vd_last_packed_passes(vd_handle h, uint32_t* passes) {
   if (!passes) return VD_ERR_ARG;
   DeviceGuard guard(h->device);
   uint32_t flags[kLocSlots];
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st_ = sync_stream(h)) return st_;
   CK(cudaMemcpy(flags, h->loc, sizeof flags, cudaMemcpyDeviceToHost));
   uint32_t n = 0;
   for (const auto& p : h->loc_last)
@@ -1322,7 +1384,7 @@ vd_status vd_last_packed_passes(vd_handle h, uint32_t* passes) {
 vd_status vd_synchronize(vd_handle h) {
   CHECK_HANDLE(h);
   DeviceGuard guard(h->device);
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st_ = sync_stream(h)) return st_;
   return VD_OK;
 }
 
@@ -1335,7 +1397,7 @@ vd_status vd_set_pass_timing(vd_handle h, int enable) {
 vd_status vd_pass_timing(vd_handle h, double* ms, uint64_t* launches, uint64_t* pixels) {
   CHECK_HANDLE(h);
   DeviceGuard guard(h->device);
-  CK(cudaStreamSynchronize(h->stream));
+  if (vd_status st_ = sync_stream(h)) return st_;
   double total = 0.0;
   for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
     float t = 0.f;

@@ -761,7 +761,11 @@ __global__ void peer_wait(const uint32_t* flags, int need_top, int need_bot, uin
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       if ((int32_t)(v - seq) >= 0) break;
-      if (it > (1ll << 24)) { atomicExch(err, 1u); return; }
+      if (it > (1ll << 24)) {  // err: mapped host memory, read by the host at every libvd call
+        *(volatile uint32_t*)err = 1u;
+        __threadfence_system();
+        return;
+      }
       __nanosleep(1000);
     }
   }

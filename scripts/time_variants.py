@@ -10,6 +10,7 @@ import json, os, sys
 sys.path.insert(0, os.getcwd())
 import torch, synth
 import paper_2209_00117_b200 as vd
+vd._load_variant(os.environ['VARIANT_LIB'])
 N, s = {"C4": (16384, 1 << 20), "C3": (4096, 65536), "C5": (65536, 1 << 24)}[os.environ.get("VD_CFG", "C4")]
 xy = synth.uniform_seeds(N, s, rng_seed=2209)
 st = torch.cuda.Stream()
@@ -50,7 +51,7 @@ if len(sys.argv) > 1 and "=" in sys.argv[1]:
 else:
     runs = [(os.path.basename(l), l, {}) for l in sorted(glob.glob("build/variants/*.so")) + ["paper_2209_00117_b200/libvd.so"]]
 for name, lib, extra in runs:
-    env = dict(os.environ, VD_LIB=os.path.abspath(lib), **extra)
+    env = dict(os.environ, VARIANT_LIB=os.path.abspath(lib), **extra)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
     out = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
     print(f"{name:45s} {out}", flush=True)

@@ -23,12 +23,13 @@ def scale(r, k):  # raw CSV units row (rows[1]) may say byte / Kbyte / Mbyte / G
     return f(r, k) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
 
+TIME_MS = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}  # raw CSV time unit -> ms
 launches = []
 for r in rows[2:]:
     rd, wr = scale(r, "dram__bytes_read.sum"), scale(r, "dram__bytes_write.sum")
     launches.append({
         "kernel": r[col["Kernel Name"]], "dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes": rd + wr,
-        "ncu_ms": f(r, "gpu__time_duration.sum") / (1e6 if rows[1][col["gpu__time_duration.sum"]] == "nsecond" else 1e3),
+        "ncu_ms": f(r, "gpu__time_duration.sum") * TIME_MS[rows[1][col["gpu__time_duration.sum"]]],
         "issue_active_pct": f(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "alu_pipe_pct": f(r, "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
         "fma_pipe_pct": f(r, "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
