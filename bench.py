@@ -407,7 +407,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-exact-sample", action="store_true")
+    ap.add_argument("--no-exact", "--no-exact-sample", dest="no_exact_sample", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the dJFAm (Manhattan) measurement")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="N > 1: halo rows pushed by the pass kernels over peer memory, or NCCL send/recv")

@@ -194,13 +194,18 @@ def move(N: int, xy_old, disp) -> np.ndarray:
 
 
 def djfa_step(N: int, xy_old, disp, d_max: int, G: np.ndarray, extras: int = 0, metric: str = "euclid",
-              vn_waves: int = 0):
+              vn_waves: int = 0, inplace: bool = False):
     """One dJFA time step (Alg. 1; R-9).  Returns (G_new, xy_new, passes).
-    metric "manhattan" = dJFAm; vn_waves = Von Neumann waves first."""
+    metric "manhattan" = dJFAm; vn_waves = Von Neumann waves first.
+    inplace: advance the caller's C-contiguous uint32 array G itself instead of a copy
+    (saves one N*N copy of host memory at 65536^2; the arithmetic is the same)."""
     xy_old = _seeds(xy_old)
     disp = np.ascontiguousarray(disp, dtype=np.int16).reshape(-1)
     assert disp.size == xy_old.size
-    G = np.array(G, dtype=np.uint32, copy=True, order="C")
+    if inplace:
+        assert G.dtype == np.uint32 and G.flags["C_CONTIGUOUS"] and G.flags["WRITEABLE"]
+    else:
+        G = np.array(G, dtype=np.uint32, copy=True, order="C")
     xy_new = np.empty_like(xy_old)
     n = _load().or_djfa_step_v(N, xy_old.size // 2, _ptr(xy_old), _ptr(disp), d_max, extras, METRICS[metric],
                                vn_waves, _ptr(G), _ptr(xy_new))

@@ -64,3 +64,27 @@ def seeds_xy(fx: dict, key: str = "seeds") -> np.ndarray:
 def disp_xy(fx: dict) -> np.ndarray:
     pts = [fx["disp"][k] for k in sorted(fx["disp"])]
     return np.array([c for p in pts for c in p], dtype=np.int16)
+
+
+def load_seed_runs(name: str) -> dict:
+    """Fixtures written as `seeds old_x old_y disp_x disp_y count` runs (index order) plus
+    `expect px py lx ly` lines (pixel (px,py) ends with the label of (lx,ly))."""
+    out = {"old": [], "disp": [], "expect": []}
+    for ln in open(os.path.join(GOLDEN_DIR, name), encoding="utf-8"):
+        tok = ln.split("#", 1)[0].split()
+        if not tok:
+            continue
+        if tok[0] in ("N", "d_max"):
+            out[tok[0]] = int(tok[1])
+        elif tok[0] == "schedule":
+            out["schedule"] = [int(t) for t in tok[1:]]
+        elif tok[0] == "seeds":
+            ox, oy, dx, dy, cnt = (int(t) for t in tok[1:])
+            out["old"] += [(ox, oy)] * cnt
+            out["disp"] += [(dx, dy)] * cnt
+        elif tok[0] == "expect":
+            px, py, lx, ly = (int(t) for t in tok[1:])
+            out["expect"].append((px, py, _pack(lx, ly)))
+    out["old_xy"] = np.array([c for p in out["old"] for c in p], dtype=np.uint16)
+    out["disp_xy"] = np.array([c for p in out["disp"] for c in p], dtype=np.int16)
+    return out

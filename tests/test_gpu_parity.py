@@ -118,9 +118,28 @@ def test_djfa_bit_exact(vd, N, s, dmax):
     _djfa_run(vd, N, s, dmax, 4, N * 7 + s)
 
 
-def test_djfa_c2_prefix(vd):
-    # BASELINE.json configs[1]: 1024x1024, 1024 seeds, +-1 px moves (first 20 of 100 steps)
-    _djfa_run(vd, 1024, 1024, 1, 20, 2209)
+def test_djfa_c2_all_frames(vd):
+    # BASELINE.json configs[1]: 1024x1024, 1024 seeds, +-1 px moves, all 100 steps, every
+    # pixel of every frame compared
+    _djfa_run(vd, 1024, 1024, 1, 100, 2209)
+
+
+def test_djfa_colocated_split_golden(vd):
+    # tests/golden/djfa_colocated_split.txt (hand-worked; pins R-9's co-location rule in the
+    # oracle): the GPU step from the same previous diagram gives the fixture's labels and
+    # the oracle's whole diagram.
+    import golden_io
+    fx = golden_io.load_seed_runs("djfa_colocated_split.txt")
+    N, old, disp = fx["N"], fx["old_xy"], fx["disp_xy"]
+    prev = oracle.exact_brute(N, old)
+    d = vd.VoronoiDiagram(N, old)
+    d.set_labels(prev)
+    d.djfa_step(disp, fx["d_max"])
+    L = d.labels()
+    G, _, _ = oracle.djfa_step(N, old, disp, fx["d_max"], prev)
+    assert np.array_equal(L, G)
+    for px, py, lab in fx["expect"]:
+        assert int(L[py, px]) == lab, (px, py)
 
 
 def test_djfa_clamp_at_borders(vd):
@@ -199,10 +218,12 @@ def test_similarity_and_hash_match_oracle(vd):
     assert b.label_hash() == oracle.label_hash(B)
 
 
-def test_c3_full_size_bit_exact(vd):
-    # BASELINE.json configs[2]: 4096x4096, 65,536 seeds, +-1 px moves; JFA + 3 dJFA frames,
-    # every pixel compared.
-    _djfa_run(vd, 4096, 65536, 1, 3, 2209)
+@pytest.mark.parametrize("dmax", [1, 64])
+def test_c3_full_size_bit_exact(vd, dmax):
+    # BASELINE.json configs[2]: 4096x4096, 65,536 seeds; JFA + 10 dJFA frames at move radius
+    # 1 (6 passes) and 64 (7 passes: d_max sets delta_1), every pixel of every frame
+    # compared.
+    _djfa_run(vd, 4096, 65536, dmax, 10, 2209 + dmax)
 
 
 def test_c3_move_radius_sweep_bit_exact(vd):
@@ -216,34 +237,63 @@ def test_c3_move_radius_sweep_bit_exact(vd):
 @pytest.mark.slow
 def test_c4_bench_config_full_grid(vd):
     # BASELINE.json configs[3] at the size bench.py times (16384^2, 2^20 seeds, +-1 px), in
-    # the same launch configuration: JFA bootstrap + 2 dJFA frames, whole-diagram hash and
-    # match count against the oracle, plus properties that hold at any size.
+    # the same launch configuration: JFA bootstrap + 3 dJFA frames, every pixel of every frame
+    # compared with the oracle (np.array_equal on the host), plus properties that hold at any
+    # size.
     N, s = 16384, 1 << 20
     xy = synth.uniform_seeds(N, s, rng_seed=2209)
     d = _jfa_gpu(vd, N, xy)
     G = oracle.jfa(N, xy)
-    assert d.label_hash() == oracle.label_hash(G)
-    for f in range(2):
+    assert np.array_equal(d.labels(), G), "JFA bootstrap"
+    for f in range(3):
         disp = synth.displacements(s, 1, f, rng_seed=2209)
         d.djfa_step(disp, 1)
-        G, xy, _ = oracle.djfa_step(N, xy, disp, 1, G)
-        assert d.label_hash() == oracle.label_hash(G)
-        _, m = vd.vd_similarity_host(d.h, G)
-        assert m == N * N
+        G, xy, n = oracle.djfa_step(N, xy, disp, 1, G, inplace=True)
+        assert d.last_passes() == n == 6
+        assert d.last_packed_passes() == 6  # the bench's regime: every delta pass on the packed walk
+        L = d.labels()
+        assert np.array_equal(L, G), f
+    assert d.label_hash() == oracle.label_hash(G)
     # every seed pixel holds its own label
-    L = d.labels()
     lx, ly = xy[0::2].astype(np.int64), xy[1::2].astype(np.int64)
     assert np.array_equal(L[ly, lx], (ly.astype(np.uint32) << 16) | lx.astype(np.uint32))
-    # sampled pixels against the exact nearest seed (Eq. 1), computed one by one
-    rng = np.random.default_rng(0)
-    py, px = rng.integers(0, N, 400), rng.integers(0, N, 400)
-    good = 0
-    for y, x in zip(py, px):
-        d2 = (lx - x) ** 2 + (ly - y) ** 2
-        m = d2.min()
-        best = ((ly[d2 == m].astype(np.uint32) << 16) | lx[d2 == m].astype(np.uint32)).min()
-        good += int(L[y, x] == best)
-    assert good >= 396  # P:268 "nearly 100%"
+
+
+@pytest.mark.slow
+def test_c5_jfa_and_djfa_frames_full_grid(vd):
+    # BASELINE.json configs[4]: 65536^2 grid, 2^24 uniform seeds, +-1 px moves, one GPU, the
+    # launch configuration bench.py --config C5 times: JFA (64-bit kernel while EMPTY remains,
+    # then the large-step and windowed kernels) + 2 dJFA frames (move_fwd with a 16-GiB fwd
+    # map, remap, reset_stamp, windowed packed passes), every pixel compared with the oracle.
+    # Host memory: the oracle's map (16 GiB) + its fwd and pass buffers (32 GiB) + the GPU
+    # map (16 GiB).
+    import time
+    N, s = 65536, 1 << 24
+    xy = synth.uniform_seeds(N, s, rng_seed=2209)
+    t0 = time.perf_counter()
+    d = _jfa_gpu(vd, N, xy)
+    L = d.labels()
+    t1 = time.perf_counter()
+    G = oracle.jfa(N, xy)
+    t2 = time.perf_counter()
+    assert np.array_equal(L, G), "JFA bootstrap"
+    print(f"C5 JFA: gpu+download {t1 - t0:.1f} s, oracle {t2 - t1:.1f} s, equal", flush=True)
+    del L
+    for f in range(2):
+        disp = synth.displacements(s, 1, f, rng_seed=2209)
+        t0 = time.perf_counter()
+        d.djfa_step(disp, 1)
+        L = d.labels()
+        t1 = time.perf_counter()
+        G, xy, n = oracle.djfa_step(N, xy, disp, 1, G, inplace=True)
+        t2 = time.perf_counter()
+        assert d.last_passes() == n == 6
+        assert np.array_equal(d.seeds(), xy), f
+        assert np.array_equal(L, G), f
+        print(f"C5 dJFA frame {f}: gpu+download {t1 - t0:.1f} s, oracle {t2 - t1:.1f} s, equal, "
+              f"packed passes {d.last_packed_passes()}", flush=True)
+        del L
+    d.close()
 
 
 @pytest.mark.parametrize("N", [16384, 20000])

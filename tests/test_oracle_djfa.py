@@ -127,3 +127,30 @@ def test_djfa_similarity_denser():
     for G, xy in _simulate(256, 256, 4, 6, 7):
         sims.append(oracle.similarity(G, oracle.jfa(256, xy)))
     assert min(sims) >= 95.0 and np.mean(sims) >= 99.0
+
+
+def _quadrants(N, corners):
+    """The previous diagram of djfa_colocated_split.txt, written from its header: four
+    16x16 quadrants, labelled by the corner seed of each."""
+    (o1, q, r, o2) = corners
+    G = np.empty((N, N), dtype=np.uint32)
+    h = N // 2
+    G[:h, :h], G[:h, h:], G[h:, :h], G[h:, h:] = o1, q, r, o2
+    return G
+
+
+def test_golden_colocated_split_pins_min_rule():
+    # R-9's co-location rule (fwd[o] = min packed new position), pinned by a hand-worked
+    # case where other rules (largest, first writer, last writer) give other labels.
+    fx = golden_io.load_seed_runs("djfa_colocated_split.txt")
+    N, old, disp = fx["N"], fx["old_xy"], fx["disp_xy"]
+    s = old.size // 2
+    assert s == 258
+    assert oracle.djfa_schedule(N, s, fx["d_max"]) == fx["schedule"]
+    prev = _quadrants(N, [golden_io._pack(0, 0), golden_io._pack(31, 0), golden_io._pack(0, 31),
+                          golden_io._pack(31, 31)])
+    assert np.array_equal(oracle.exact_brute(N, old), prev)  # the header's quadrant claim (Eq. 1)
+    G, new, n = oracle.djfa_step(N, old, disp, fx["d_max"], prev)
+    assert n == 3
+    for px, py, lab in fx["expect"]:
+        assert int(G[py, px]) == lab, (px, py, hex(int(G[py, px])), hex(lab))
