@@ -48,8 +48,8 @@ CONFIGS = {
     "C5": (65536, 1 << 24, 1, "65536x65536 grid, 2^24 uniform seeds, +-1 px uniform moves"),
 }
 RNG = synth.RNG_SEED
-# bounded CPU sample: same seed density (L_avg = 16) and move radius, 4096^2 grid
-CPU_SAMPLE = (4096, 65536, 1)
+NOMINAL_HBM_GBS = 8000.0  # the north star's "B200 peak of about 8 TB/s"
+CPU_FRAMES = 3            # timed oracle frames for cpu_baseline (after the untimed bootstrap)
 
 
 def _peaks():
@@ -126,45 +126,62 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------- CPU oracle leg
 
-def cpu_oracle_sample(steps: int, warmup: int, budget_s: float | None, target_n: int):
-    """Time the oracle's literal dJFA on the bounded sample.  Returns (frames/s scaled to
-    the target grid, Gpix.pass/s, description, threads, frames timed)."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_run(N: int, xy0, disps, d: int, warmup: int, check=None):
+    """The CPU oracle on the bench workload itself (the same grid, seeds and displacement
+    stream as the GPU): JFA bootstrap (untimed), `warmup` untimed dJFA frames, then one
+    timed dJFA frame (oracle.djfa_step: move + fwd map + remap + re-stamp + passes, the same
+    region the GPU step covers) per remaining entry of `disps`.  check(stage, G) is called on
+    the bootstrap (stage 0) and after every frame (stage f + 1), untimed.
+    Returns (ms per timed frame, passes per frame, threads)."""
     import oracle
-    n, s, d = CPU_SAMPLE
-    xy = synth.uniform_seeds(n, s, rng_seed=RNG)
-    G = oracle.jfa(n, xy)
-    passes = len(oracle.djfa_schedule(n, s, d))
-    for f in range(warmup):
-        G, xy, _ = oracle.djfa_step(n, xy, synth.displacements(s, d, f, rng_seed=RNG), d, G)
-    frames, t0 = 0, time.perf_counter()
-    while frames < steps:
-        G, xy, _ = oracle.djfa_step(n, xy, synth.displacements(s, d, warmup + frames, rng_seed=RNG), d, G)
-        frames += 1
-        if budget_s is not None and time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    fps_sample = frames / dt
-    scale = (n * n) / float(target_n * target_n)
-    desc = (f"oracle dJFA (fwd map + remap + stamp + {passes} passes) on a {n}x{n} grid with {s} seeds "
-            f"(same density L_avg=16 and +-{d} px moves as the bench grid), {frames} frames in {dt:.1f} s; "
-            f"frames/s scaled by pixel ratio {n}^2/{target_n}^2")
-    return fps_sample * scale, n * n * passes * fps_sample / 1e9, desc, oracle.num_threads(), frames
+    G = oracle.jfa(N, xy0)
+    if check:
+        check(0, G)
+    xy = xy0
+    times, passes = [], 0
+    for f, disp in enumerate(disps):
+        t0 = time.perf_counter()
+        G, xy, passes = oracle.djfa_step(N, xy, disp, d, G, inplace=True)
+        dt = time.perf_counter() - t0
+        if f >= warmup:
+            times.append(dt)
+        if check:
+            check(f + 1, G)
+    return [1000.0 * t for t in times], passes, oracle.num_threads()
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    N, s, d, _ = CONFIGS[args.config]
-    fps, gpps, desc, threads, frames = cpu_oracle_sample(args.steps, args.warmup, None, N)
+    N, s, d, cdesc = CONFIGS[args.config]
+    xy0 = synth.uniform_seeds(N, s, rng_seed=RNG)
+    W, K = args.warmup, args.steps
+    disps = [synth.displacements(s, d, f, rng_seed=RNG) for f in range(W + K)]
+    ms, passes, threads = oracle_run(N, xy0, disps, d, W)
+    mean_ms = sum(ms) / len(ms)
+    fps = 1000.0 / mean_ms
+    sample = (f"oracle/ (plain C + OpenMP, uint64 keys) on the bench workload itself: {N}x{N} grid, {s} seeds, "
+              f"+-{d} px moves; JFA bootstrap and {W} warm-up frames untimed, then {K} dJFA frames timed one by one "
+              f"(move + fwd map + remap + re-stamp + {passes} passes each); CPU: {cpu_model()}")
     line = {
         "impl": "reference", "metric": "dJFA frames/s", "value": fps, "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": frames, "warmup": args.warmup, "ms_per_step": 1000.0 / fps,
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": mean_ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "gpix_pass_per_s": gpps,
-        "config": {"workload": f"{args.config}: {CONFIGS[args.config][3]} (bounded CPU sample, see cpu_baseline)",
-                   "N": N, "seeds": s, "d_max": d},
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "data": "synthetic", "gpix_pass_per_s": N * N * passes / (mean_ms / 1000.0) / 1e9,
+        "config": {"workload": f"{args.config}: {cdesc}, dJFA time steps", "N": N, "seeds": s, "d_max": d},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -204,7 +221,15 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather(obj):
+        if world == 1:
+            return [obj]
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
     N, s, d, cdesc = CONFIGS[args.config]
+    B = N // world
 
     def handle_cfg():
         # every libvd handle gets its own NCCL communicator, hence its own unique id
@@ -238,9 +263,25 @@ def run_gpu(args):
     disp_host = [synth.displacements(s, d, f, rng_seed=RNG) for f in range(nframes)]
     disp_dev = torch.from_numpy(np.stack(disp_host[: W + K])).to("cuda")  # resident in HBM
     disp_pin = [torch.from_numpy(a).pin_memory() for a in disp_host[W + K:]]
+    peak, peak_src = _peaks()
 
     def ev():
         return torch.cuda.Event(enable_timing=True)
+
+    def roofline(times, kernel):
+        """times: [(k, ms)] of timed jump passes (all launches of a pass); 8 B/px/pass algorithmic."""
+        tot_ms = sum(t for _, t in times)
+        n = max(len(times), 1)
+        alg = 8.0 * B * N  # bytes per pass per rank (one band)
+        ach = alg * n / (tot_ms / 1000.0) / 1e9 if tot_ms else 0.0
+        per_k = {}
+        for k, t in times:
+            per_k.setdefault(k, []).append(t)
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "frac_nominal": ach / NOMINAL_HBM_GBS, "kernel": kernel, "alg_bytes_per_launch": alg,
+                "avg_launch_ms": tot_ms / n, "launches_timed": len(times), "peak_source": peak_src,
+                "per_k": {str(k): {"ms": statistics.mean(v), "frac": alg / (statistics.mean(v) / 1000.0) / 1e9 / peak}
+                          for k, v in sorted(per_k.items(), reverse=True)}}
 
     # ---------------- dJFA: bootstrap (untimed), warmup, timed region
     dj = make()
@@ -264,20 +305,26 @@ def run_gpu(args):
         torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    own_ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(own_ms)
     dj.set_pass_timing(False)
+    dj_times = dj.pass_times()
     pass_ms, pass_launches, pass_px = dj.pass_timing()
     launches = dj.launch_count() - launches0
+    if world > 1:
+        assert not dj.peer_timed_out(), "a peer-halo wait timed out during the timed region"
     fps = K / (ms / 1000.0)
     gpps = N * N * passes * K / (ms / 1000.0) / 1e9
+    per_rank = gather({"rank": rank, "frame_ms": own_ms / K, "pass_ms": pass_ms / K,
+                       "other_ms": (own_ms - pass_ms) / K})
 
     # ---------------- JFA baseline on the same frames (move + full JFA each frame)
     for f in range(W):
         jf.move_seeds(disp_dev[f])
         jf.jfa()
-    jpasses = None
     torch.cuda.synchronize()
     barrier()
+    jf.set_pass_timing(True)
     j0, j1 = ev(), ev()
     j0.record(stream)
     for f in range(W, W + K):
@@ -287,6 +334,9 @@ def run_gpu(args):
     torch.cuda.synchronize()
     barrier()
     jms = max_over_ranks(j0.elapsed_time(j1))
+    jf.set_pass_timing(False)
+    jf_times = jf.pass_times()
+    jf.pass_timing()
     jpasses = jf.last_passes()
     jpacked = jf.last_packed_passes()
     jfps = K / (jms / 1000.0)
@@ -315,24 +365,22 @@ def run_gpu(args):
                "paper": "dJFAm ~5x over JFA at 88-92% similarity (P:268, P:296; A100)"}
         dm.close()
 
-    # similarity vs the exact diagram on sampled pixels (Eq. 1 by brute force per pixel)
+    # ---------------- Eq. 5 similarity of each method vs the exact diagram (Eq. 1), whole grid
+    # (untimed; the exact diagram is the oracle's bucketed brute force on this frame's seeds)
     sim_exact = None
-    if rank == 0 and world == 1 and not args.no_exact_sample:
-        L = dj.labels()
-        cur = dj.seeds()
-        lx, ly = cur[0::2].astype(np.int64), cur[1::2].astype(np.int64)
-        lab = (ly.astype(np.uint64) << np.uint64(16)) | lx.astype(np.uint64)
-        rng = np.random.default_rng(1)
-        good, n_s = 0, 200
-        for y, x in zip(rng.integers(0, N, n_s), rng.integers(0, N, n_s)):
-            d2 = (lx - x) ** 2 + (ly - y) ** 2
-            good += int(L[y, x] == lab[d2 == d2.min()].min())
-        sim_exact = {"pct": 100.0 * good / n_s, "pixels": n_s}
+    if rank == 0 and world == 1 and not args.no_exact:
+        import oracle
+        t0 = time.perf_counter()
+        E = oracle.exact(N, dj.seeds())
+        sim_exact = {"djfa_pct": dj.similarity_host(E), "jfa_pct": jf.similarity_host(E), "pixels": N * N,
+                     "frame": W + K, "exact": f"oracle.exact (bucketed brute force, Eq. 1), {time.perf_counter() - t0:.1f} s"}
+        if djm is not None:
+            sim_exact["note"] = "dJFAm is compared with the Euclidean JFA only (R-23)"
+        del E
 
     # ---------------- end to end: host (pinned) displacements in, 8-byte hash out
     barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     x0, x1 = ev(), ev()
     hashes = torch.zeros(len(disp_pin), dtype=torch.int64).pin_memory()  # each step's result
     x0.record(stream)
@@ -344,51 +392,93 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(x0.elapsed_time(x1))
     assert int(hashes[-1]) & 0xFFFFFFFFFFFFFFFF == dj.label_hash(), "async checksum mismatch"
     e2e_fps = len(disp_pin) / (e2e_ms / 1000.0)
+    # ... and with the whole label map (this rank's band) copied to pinned host memory each step
+    e2e_full = None
+    if not args.no_e2e_full:
+        out = torch.empty((B, N), dtype=torch.int32).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for a in disp_pin:
+            vd.vd_djfa_step(dj.h, a, d, s)
+            vd.vd_get_labels_into(dj.h, out.data_ptr())
+        full_s = max_over_ranks(time.perf_counter() - t0)
+        e2e_full = {"value": len(disp_pin) / full_s, "unit": "frames/s", "h2d_bytes_per_step": 4 * s,
+                    "d2h_bytes_per_step": 4 * B * N, "steps": len(disp_pin),
+                    "what": "vd_djfa_step with pinned host displacements + vd_get_labels of the whole label map "
+                            "into pinned host memory (synchronous) per step; host wall clock"}
 
-    # ---------------- roofline of the dominant kernel (the jump pass)
-    peak, peak_src = _peaks()
-    alg_bytes = 8.0 * pass_px / max(pass_launches, 1)
-    pass_avg_ms = pass_ms / max(pass_launches, 1)
-    achieved = alg_bytes / (pass_avg_ms / 1000.0) / 1e9
-    frame_share = pass_ms / (ms if world == 1 else pass_ms + 1e-9)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": _traffic_per_launch(args.config), "kernel": "jump_pass_fast",
-                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": pass_avg_ms,
-                "launches_timed": pass_launches, "share_of_step": frame_share if world == 1 else None,
-                "peak_source": peak_src}
+    # ---------------- parity of the timed path (untimed): the JFA bootstrap and the first
+    # CPU_FRAMES dJFA frames of this workload, GPU vs the CPU oracle.  One GPU: every pixel
+    # (np.array_equal); N > 1: the all-reduced whole-diagram label hash on rank 0.
+    pv = make()
+    pv.jfa()
+    gpu_stages = [(pv.label_hash(), pv.labels() if world == 1 else None)]
+    for f in range(CPU_FRAMES):
+        pv.djfa_step(disp_host[f], d)
+        gpu_stages.append((pv.label_hash(), pv.labels() if world == 1 else None))
+    pv.close()
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        ok = []
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cfps, cgpps, cdesc2, threads, _ = cpu_oracle_sample(10**6, 1, args.cpu_seconds, N)
-        cpu = {"value": cfps, "unit": "frames/s", "cores": threads, "kind": "oracle", "sample": cdesc2,
-               "gpix_pass_per_s": cgpps}
+        def check(stage, G):
+            h, L = gpu_stages[stage]
+            ok.append(bool(np.array_equal(L, G)) if L is not None else h == oracle.label_hash(G))
 
+        cms, cpasses, threads = oracle_run(N, xy0, disp_host[:CPU_FRAMES], d, 0, check)
+        cmean = sum(cms) / len(cms)
+        parity = {"ok": all(ok), "stages": ok,
+                  "what": ("JFA bootstrap + dJFA frames 1..%d of this workload: GPU %s vs the CPU oracle"
+                           % (CPU_FRAMES, "label map == oracle map (every pixel)" if world == 1
+                              else "all-reduced label hash == oracle label hash"))}
+        if world == 1:
+            cpu = {"value": 1000.0 / cmean, "unit": "frames/s", "cores": threads, "kind": "oracle",
+                   "sample": (f"the bench workload itself ({N}x{N}, {s} seeds, +-{d} px): oracle JFA bootstrap "
+                              f"untimed, then {CPU_FRAMES} dJFA frames timed one by one (move + fwd map + remap + "
+                              f"re-stamp + {cpasses} passes), {cmean / 1000.0:.2f} s per frame"),
+                   "cpu_model": cpu_model(), "gpix_pass_per_s": N * N * cpasses / (cmean / 1000.0) / 1e9,
+                   "ms_per_frame": cmean}
+    barrier()
+
+    dj_roof = roofline(dj_times, "jump_pass_fast (packed-key walk)")
+    dj_roof["traffic"] = _traffic_per_launch(args.config)
+    dj_roof["share_of_step"] = pass_ms / own_ms
+    jf_roof = roofline(jf_times, "jump_pass_fast (exact walk) / jump_pass_wide")
     if rank == 0:
         line = {
             "metric": "dJFA frames/s", "value": fps, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"{args.config}: {cdesc}, dJFA time steps", "N": N, "seeds": s, "d_max": d,
-                       "passes_per_frame": passes, "packed_passes_per_frame": packed, "parallelism": f"rowband{world}", "halo": halo_mode[0],
+                       "passes_per_frame": passes, "packed_passes_per_frame": packed, "parallelism": f"rowband{world}",
+                       "halo": halo_mode[0],
                        "l2": (f"inputs larger than L2 (two {4 * N * N / 2**30:g}-GiB ping-pong label buffers vs 126 MB L2)"
                               if 8 * N * N > 126e6 else "inputs fit in L2, no flush: a parity config, not the headline")},
             "gpix_pass_per_s": gpps,
             "jfa": {"value": jfps, "unit": "frames/s", "ms_per_frame": jms / K, "passes_per_frame": jpasses,
                     "packed_passes_per_frame": jpacked,
-                    "gpix_pass_per_s": N * N * jpasses * K / (jms / 1000.0) / 1e9},
+                    "gpix_pass_per_s": N * N * jpasses * K / (jms / 1000.0) / 1e9, "roofline": jf_roof},
             "speedup_vs_jfa": jfps and fps / jfps,
             "similarity_vs_jfa_pct": sim_vs_jfa,
-            "similarity_vs_exact_sampled": sim_exact,
+            "similarity_vs_exact": sim_exact,
             "djfam": djm,
             "paper_context": "A100 40GB (P:222-240): dJFA up to ~5.3x over JFA, similarity >= 88% (P:25)",
-            "roofline": roofline,
+            "roofline": dj_roof,
+            "parity": parity,
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 4 * s, "d2h_bytes_per_step": 8,
                     "steps": len(disp_pin),
-                    "what": "vd_djfa_step with pinned host displacements + vd_label_hash_async (8-byte D2H into pinned memory, no per-step host round trip) per step"},
+                    "what": ("vd_djfa_step with pinned host displacements + vd_label_hash_async per step; the step's "
+                             "result read back is an 8-byte checksum of the whole label map (a consumer of the map "
+                             "itself: see e2e_full_map)")},
+            "e2e_full_map": e2e_full,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        if world > 1:
+            line["per_rank"] = per_rank
         print(json.dumps(line), flush=True)
     dj.close()
     jf.close()
@@ -405,9 +495,9 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=30)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-exact", "--no-exact-sample", dest="no_exact_sample", action="store_true")
+    ap.add_argument("--no-e2e-full", action="store_true", help="skip the e2e run that copies the whole map out")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU oracle (cpu_baseline and parity)")
+    ap.add_argument("--no-exact", action="store_true", help="skip the whole-grid similarity vs the exact diagram")
     ap.add_argument("--no-variants", action="store_true", help="skip the dJFAm (Manhattan) measurement")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="N > 1: halo rows pushed by the pass kernels over peer memory, or NCCL send/recv")

@@ -219,6 +219,10 @@ vd_status vd_synchronize(vd_handle h);
  * of timed launches and the pixels they covered, then resets the accumulators. */
 vd_status vd_set_pass_timing(vd_handle h, int enable);
 vd_status vd_pass_timing(vd_handle h, double* ms, uint64_t* launches, uint64_t* pixels);
+/* The timed intervals accumulated since the last vd_pass_timing, one per jump pass (all of
+ * its launches): device time ms[i] and step ks[i], for i < min(*n, cap); *n = how many
+ * there are.  Does not reset (vd_pass_timing does).  ms / ks may be NULL. */
+vd_status vd_pass_times(vd_handle h, float* ms, uint32_t* ks, uint32_t cap, uint32_t* n);
 
 /* Number of kernels this handle has launched since creation. */
 vd_status vd_launch_count(vd_handle h, uint64_t* n);

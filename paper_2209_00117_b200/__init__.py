@@ -21,9 +21,9 @@ import numpy as np
 __all__ = [
     "VDError", "load_library", "library_path", "VoronoiDiagram", "EMPTY",
     "vd_config", "vd_halo_plan_t", "vd_create", "vd_destroy", "vd_jfa", "vd_move_seeds",
-    "vd_djfa_step", "vd_stf", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
+    "vd_djfa_step", "vd_stf", "vd_get_labels_into", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
     "vd_get_seeds", "vd_band", "vd_last_passes", "vd_last_packed_passes", "vd_synchronize", "vd_set_pass_timing",
-    "vd_pass_timing", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
+    "vd_pass_timing", "vd_pass_times", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
     "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "vd_peer_export",
     "vd_peer_attach", "vd_peer_status", "vd_label_hash_async", "EXPORTED_SYMBOLS",
 ]
@@ -98,6 +98,7 @@ _SIGS = {
     "vd_set_pass_timing": (ctypes.c_int32, [H, ctypes.c_int]),
     "vd_pass_timing": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64),
                                         ctypes.POINTER(ctypes.c_uint64)]),
+    "vd_pass_times": (ctypes.c_int32, [H, P, P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]),
     "vd_launch_count": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint64)]),
     "vd_schedule_jfa": (ctypes.c_int32, [ctypes.c_uint32, ctypes.c_uint32, P, ctypes.c_uint32,
                                          ctypes.POINTER(ctypes.c_uint32)]),
@@ -310,6 +311,12 @@ def vd_get_labels(h, N: int) -> np.ndarray:
     return out
 
 
+def vd_get_labels_into(h, ptr: int) -> None:
+    """vd_get_labels into caller memory at address ptr (e.g. a pinned torch tensor's
+    data_ptr(), rows x N uint32 of this handle's band)."""
+    _check(load_library().vd_get_labels(h, ctypes.c_void_p(ptr)), "vd_get_labels", h)
+
+
 def vd_get_seeds(h, s: int) -> np.ndarray:
     out = np.empty(2 * s, dtype=np.uint16)
     _check(load_library().vd_get_seeds(h, ctypes.c_void_p(out.ctypes.data)), "vd_get_seeds", h)
@@ -341,6 +348,18 @@ def vd_pass_timing(h) -> tuple[float, int, int]:
     _check(load_library().vd_pass_timing(h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(px)),
            "vd_pass_timing", h)
     return ms.value, n.value, px.value
+
+
+def vd_pass_times(h) -> list[tuple[int, float]]:
+    """(k, ms) of every timed jump pass since the last vd_pass_timing (no reset)."""
+    lib = load_library()
+    n = ctypes.c_uint32()
+    _check(lib.vd_pass_times(h, None, None, 0, ctypes.byref(n)), "vd_pass_times", h)
+    ms = np.zeros(n.value, dtype=np.float32)
+    ks = np.zeros(n.value, dtype=np.uint32)
+    _check(lib.vd_pass_times(h, ctypes.c_void_p(ms.ctypes.data), ctypes.c_void_p(ks.ctypes.data), n.value,
+                             ctypes.byref(n)), "vd_pass_times", h)
+    return [(int(k), float(t)) for k, t in zip(ks, ms)]
 
 
 def vd_launch_count(h) -> int:
@@ -470,6 +489,9 @@ class VoronoiDiagram:
 
     def pass_timing(self):
         return vd_pass_timing(self.h)
+
+    def pass_times(self):
+        return vd_pass_times(self.h)
 
     def launch_count(self) -> int:
         return vd_launch_count(self.h)

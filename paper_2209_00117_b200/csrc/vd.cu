@@ -176,6 +176,7 @@ struct vd_ctx {
   // instrumentation
   bool timing = false;
   std::vector<cudaEvent_t> ev;
+  std::vector<uint32_t> ev_k;  // step k of each timed interval
   size_t ev_used = 0;
   uint64_t timed_px = 0, timed_launches = 0;
   // NCCL
@@ -369,9 +370,11 @@ vd_status timed_begin(vd_ctx* h) {
   CK(cudaEventRecord(h->ev[h->ev_used], h->stream));
   return VD_OK;
 }
-vd_status timed_end(vd_ctx* h, uint64_t px) {
+vd_status timed_end(vd_ctx* h, uint64_t px, uint32_t k) {
   if (!h->timing) return VD_OK;
   CK(cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+  h->ev_k.resize(h->ev_used / 2 + 1);
+  h->ev_k[h->ev_used / 2] = k;
   h->ev_used += 2;
   h->timed_px += px;
   h->timed_launches++;
@@ -416,6 +419,33 @@ cudaError_t launch_fast_k(int dev, bool me, bool bd, bool rel, int metric, bool 
                     : launch_fast_mv<KM, true, false, false>(dev, metric, vn, a, g, b, sm, st);
   return bd ? launch_fast_mv<KM, false, true, false>(dev, metric, vn, a, g, b, sm, st)
             : launch_fast_mv<KM, false, false, false>(dev, metric, vn, a, g, b, sm, st);
+}
+
+// Shared-term kernel (jump_pass_sk): one band or banded, Euclidean Moore, N % 512 == 0, and
+// k in {1, 2} (adjacent columns) or 32 <= k <= N/4 (stride columns).  VD_NO_SK=1 disables it
+// (A/B timing).
+bool sk_ok(const vd_ctx* h, uint32_t k, bool vn, bool rel) {
+  static const bool off = [] { const char* e = getenv("VD_NO_SK"); return e && e[0] == '1'; }();
+  return !off && !rel && !vn && h->metric == 0 && h->N % 512 == 0 && (k <= 2 || (k >= 32 && 4 * k <= h->N));
+}
+
+template <int KM, bool ME, bool BD>
+cudaError_t launch_sk(int dev, const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
+  static std::atomic<uint64_t> opted{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(opted.load(std::memory_order_acquire) & bit)) {
+    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk<KM, ME, BD>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, vdk::kSmemBudget);
+    if (e != cudaSuccess) return e;
+    opted.fetch_or(bit, std::memory_order_release);
+  }
+  vdk::jump_pass_sk<KM, ME, BD><<<grid, blk, sm, st>>>(a);
+  return cudaSuccess;
+}
+template <int KM>
+cudaError_t launch_sk_k(int dev, bool me, bool bd, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
+  if (me) return bd ? launch_sk<KM, true, true>(dev, a, g, b, sm, st) : launch_sk<KM, true, false>(dev, a, g, b, sm, st);
+  return bd ? launch_sk<KM, false, true>(dev, a, g, b, sm, st) : launch_sk<KM, false, false>(dev, a, g, b, sm, st);
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
@@ -473,7 +503,8 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   if ((fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, R);
     const uint32_t per_res = (R + k - 1) / k;
-    a.walk = vdk::walk_len((int)k, rel);
+    const bool sk = sk_ok(h, k, vn, rel);
+    a.walk = sk ? vdk::walk_len_sk((int)k) : vdk::walk_len((int)k, rel);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     // Small grids (C2: 1024^2 at k = 1 is 2 x 1 x 43 walks of 24 rows): shorten the walks until
     // there are about two waves of resident CTAs, else a few long walks leave SMs idle.
@@ -499,9 +530,13 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     } else {
       h->pass_loc_ok = false;
     }
-    const size_t sm = vdk::pass_smem((int)k, rel);
+    const size_t sm = sk ? vdk::pass_smem_sk((int)k) : vdk::pass_smem((int)k, rel);
     cudaError_t e;
-    if (k == 1) e = launch_fast_k<1>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    if (sk) {
+      if (k == 1) e = launch_sk_k<1>(h->device, may_empty, banded, a, grid, blk, sm, h->stream);
+      else if (k == 2) e = launch_sk_k<2>(h->device, may_empty, banded, a, grid, blk, sm, h->stream);
+      else e = launch_sk_k<4>(h->device, may_empty, banded, a, grid, blk, sm, h->stream);
+    } else if (k == 1) e = launch_fast_k<1>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     else if (k == 2) e = launch_fast_k<2>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     else e = launch_fast_k<4>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     CK(e);
@@ -590,7 +625,7 @@ vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t
     for (auto& sh : h->shards) {
       if ((st = timed_begin(h))) return st;
       if ((st = launch_pass(h, sh, k, may_empty, vn))) return st;
-      if ((st = timed_end(h, (uint64_t)sh.rows * h->N))) return st;
+      if ((st = timed_end(h, (uint64_t)sh.rows * h->N, k))) return st;
     }
     h->pushed_k = 0;
     h->hpar ^= 1;
@@ -652,7 +687,7 @@ vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t
     vdk::peer_signal<<<1, 1, 0, h->stream>>>(h->nbr_flag_above, h->nbr_flag_below, seq + 1);
     if ((st = after_launch(h, "peer_signal"))) return st;
   }
-  if ((st = timed_end(h, px))) return st;
+  if ((st = timed_end(h, px, k))) return st;
   h->pushed_k = push_next ? k_next : 0;
   h->hpar ^= 1;
   h->cur ^= 1;
@@ -1410,6 +1445,22 @@ vd_status vd_pass_timing(vd_handle h, double* ms, uint64_t* launches, uint64_t* 
   h->ev_used = 0;
   h->timed_launches = 0;
   h->timed_px = 0;
+  return VD_OK;
+}
+
+vd_status vd_pass_times(vd_handle h, float* ms, uint32_t* ks, uint32_t cap, uint32_t* n) {
+  CHECK_HANDLE(h);
+  if (!n) return VD_ERR_ARG;
+  DeviceGuard guard(h->device);
+  if (vd_status st_ = sync_stream(h)) return st_;
+  const uint32_t cnt = (uint32_t)(h->ev_used / 2);
+  *n = cnt;
+  for (uint32_t i = 0; i < cnt && i < cap; ++i) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]));
+    if (ms) ms[i] = t;
+    if (ks) ks[i] = h->ev_k[i];
+  }
   return VD_OK;
 }
 

@@ -671,6 +671,339 @@ __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLO
   else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN, REL, false>(a, x0, y0, dyn_smem);
 }
 
+// ------------------------------------------------------------------ shared-term jump pass (r02)
+//
+// The pass of jump_pass_fast (Euclidean, Moore, N % 512 == 0), with the per-row terms of each
+// staged label computed ONCE for all the outputs of the thread that use it.  A label at column
+// cx serves output column X as its left neighbour (X = cx + k), centre (X = cx) or right
+// neighbour (X = cx - k); the three terms differ only through dx = cx - X:
+//   exact:  q(dx) = cy^2 + dx^2;             q(dx -+ k) = q(dx) + k^2 -+ 2k dx
+//   packed: Qk(dx) = (cy^2 + dx^2) 2^16 + dx; Qk(dx -+ k) = Qk(dx) + k^2 2^16 -+ k -+ 2k 2^16 dx
+// so each further use costs one add + one IMAD instead of a six-instruction row build.
+// Threads own columns so that the uses of a label fall in ONE thread:
+//  * KS = k in {1, 2} ("adjacent"): columns X..X+3 (X = x0 + 4t) as in jump_pass_fast; label
+//    slots s = 0 .. 3+2k hold columns X - k + s, read as three 128-bit vectors.
+//  * k >= 32 ("stride", KS = 1): columns X, X+k, X+2k, X+3k, consecutive threads on
+//    consecutive X (coalesced 32-bit stores); slots s = 0..5 hold columns X + (s-1) k.
+//    k <= 128: a CTA covers the 512 contiguous columns [x0, x0+512) in groups of 4k;
+//    k >= 256: it covers four 128-column spans x0 + j k + [0, 128), j = 0..3, and stages six
+//    spans (j = -1..4) per row instead of jump_pass_fast's three 512-wide ones.
+// Output e of the thread takes L = slot e, C = slot e + KS, R = slot e + 2 KS.  Results are
+// identical to jump_pass_fast (same keys, same minimum); only the instruction count changes.
+template <int NS>
+struct RowS {
+  uint32_t c[NS];  // labels (exact walk only)
+  int32_t cy[NS];  // c >> 16
+  int32_t qL[kVec], qC[kVec], qR[kVec];  // per output: the term of its L / C / R candidate
+};
+
+__host__ __device__ inline int stage_elems_sk(int k) { return k >= 256 ? 6 * 128 : stage_elems(k); }
+__host__ __device__ inline int walk_len_sk(int k) {
+  const int rows = kSmemBudget / (stage_elems_sk(k) * 4 + 8);
+  return rows - 2 < 1 ? 1 : (rows - 2 > kMaxWalk ? kMaxWalk : rows - 2);
+}
+__host__ __device__ inline size_t pass_smem_sk(int k) {
+  return (size_t)(walk_len_sk(k) + 2) * (stage_elems_sk(k) * 4 + 8);
+}
+
+// Row build from the NS slot labels.  xs_home[s]: -(column of slot s) << 16 (+1 for PACK);
+// xs_out[e]: the same for output column e (single-use edge slots are computed against it).
+// kk = (k^2, 2k) for the exact walk, (k^2 2^16 - k, k^2 2^16 + k, 2k 2^16) for the packed one.
+template <int KS, bool MAY_EMPTY, bool PACK>
+__device__ __forceinline__ void build_sk(uint32_t (&lab)[4 + 2 * KS], const int (&xs_home)[4 + 2 * KS],
+                                         const int (&xs_out)[kVec], uint32_t vempty, uint32_t sh16, uint32_t k2,
+                                         uint32_t m1, uint32_t m2, uint32_t m3, RowS<4 + 2 * KS>& R) {
+  constexpr int NS = 4 + 2 * KS;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    uint32_t c = lab[s];
+    if constexpr (MAY_EMPTY && !PACK) c = __vminu2(c, vempty);  // EMPTY -> virtual far seed
+    const bool hasL = s <= 3, hasC = s - KS >= 0 && s - KS <= 3, hasR = s - 2 * KS >= 0;
+    const uint32_t cy = c >> 16;
+    if constexpr (!PACK) R.c[s] = c;
+    R.cy[s] = (int)cy;
+    if constexpr (!PACK) {
+      if (hasC) {
+        const uint32_t D = c * sh16 + (uint32_t)xs_home[s];
+        const uint32_t dx = (uint32_t)((int)D >> 16);
+        const uint32_t q = dx * dx + cy * cy;
+        R.qC[s - KS] = (int)q;
+        const uint32_t t = q + k2;  // q(dx -+ k) = q + k^2 -+ 2k dx
+        if (hasL) R.qL[s] = (int)(t - m1 * dx);
+        if (hasR) R.qR[s - 2 * KS] = (int)(t + m1 * dx);
+      } else {
+        const int e = hasL ? s : s - 2 * KS;
+        const uint32_t D = c * sh16 + (uint32_t)xs_out[e];
+        const uint32_t dx = (uint32_t)((int)D >> 16);
+        const uint32_t q = dx * dx + cy * cy;
+        if (hasL) R.qL[e] = (int)q;
+        else R.qR[e] = (int)q;
+      }
+    } else {
+      const uint32_t chi = c & 0xFFFF0000u;  // cy << 16
+      if (hasC) {
+        const uint32_t D1 = c * sh16 + (uint32_t)xs_home[s];  // (cx - X) << 16 | 1
+        const uint32_t dx = (uint32_t)((int)D1 >> 16);
+        const uint32_t Qk = dx * D1 + cy * chi;                 // (dx^2 + cy^2) << 16 + dx
+        R.qC[s - KS] = (int)Qk;
+        if (hasL) R.qL[s] = (int)((Qk + k2) - m3 * dx);        // k2 = k^2 2^16 - k
+        if (hasR) R.qR[s - 2 * KS] = (int)((Qk + m1) + m3 * dx);  // m1 = k^2 2^16 + k
+      } else {
+        const int e = hasL ? s : s - 2 * KS;
+        const uint32_t D1 = c * sh16 + (uint32_t)xs_out[e];
+        const uint32_t dx = (uint32_t)((int)D1 >> 16);
+        const uint32_t Qk = dx * D1 + cy * chi;
+        if (hasL) R.qL[e] = (int)Qk;
+        else R.qR[e] = (int)Qk;
+      }
+    }
+    (void)m2;
+  }
+}
+
+template <int KS>
+__device__ __forceinline__ uint32_t best_sk(const RowS<4 + 2 * KS>& A, const RowS<4 + 2 * KS>& B,
+                                            const RowS<4 + 2 * KS>& Cn, int e, int y, int& mo) {
+  uint32_t c[9];
+  int d[9];
+  const uint32_t m2y = (uint32_t)(-2 * y);
+  auto put = [&](const RowS<4 + 2 * KS>& R, int j) {
+    c[3 * j + 0] = R.c[e];          d[3 * j + 0] = (int)((uint32_t)R.qL[e] + (uint32_t)R.cy[e] * m2y);
+    c[3 * j + 1] = R.c[e + KS];     d[3 * j + 1] = (int)((uint32_t)R.qC[e] + (uint32_t)R.cy[e + KS] * m2y);
+    c[3 * j + 2] = R.c[e + 2 * KS]; d[3 * j + 2] = (int)((uint32_t)R.qR[e] + (uint32_t)R.cy[e + 2 * KS] * m2y);
+  };
+  put(A, 0);
+  put(B, 1);
+  put(Cn, 2);
+  const int m = __vimin3_s32(__vimin3_s32(d[0], d[1], d[2]), __vimin3_s32(d[3], d[4], d[5]),
+                             __vimin3_s32(d[6], d[7], d[8]));
+  mo = m;
+  uint32_t w[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) w[i] = __viaddmax_u32((uint32_t)m, 0u - (uint32_t)d[i], c[i]);
+  return __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]), __vimin3_u32(w[6], w[7], w[8]));
+}
+
+template <bool SIGNED, int KS>
+__device__ __forceinline__ uint32_t min9_sk(const RowS<4 + 2 * KS>& A, const RowS<4 + 2 * KS>& B,
+                                            const RowS<4 + 2 * KS>& Cn, int e, uint32_t My) {
+  uint32_t kk[9];
+  auto put = [&](const RowS<4 + 2 * KS>& R, int j) {
+    kk[3 * j + 0] = (uint32_t)R.qL[e] + (uint32_t)R.cy[e] * My;
+    kk[3 * j + 1] = (uint32_t)R.qC[e] + (uint32_t)R.cy[e + KS] * My;
+    kk[3 * j + 2] = (uint32_t)R.qR[e] + (uint32_t)R.cy[e + 2 * KS] * My;
+  };
+  put(A, 0);
+  put(B, 1);
+  put(Cn, 2);
+  if constexpr (SIGNED)
+    return (uint32_t)__vimin3_s32(__vimin3_s32((int)kk[0], (int)kk[1], (int)kk[2]),
+                                  __vimin3_s32((int)kk[3], (int)kk[4], (int)kk[5]),
+                                  __vimin3_s32((int)kk[6], (int)kk[7], (int)kk[8]));
+  else
+    return __vimin3_u32(__vimin3_u32(kk[0], kk[1], kk[2]), __vimin3_u32(kk[3], kk[4], kk[5]),
+                        __vimin3_u32(kk[6], kk[7], kk[8]));
+}
+
+// One CTA walk of the shared-term pass (see walk() for the staging and the walk structure).
+// KM: 1 or 2 (adjacent, KS = k), 4 (stride, k >= 32, KS = 1).
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK>
+__device__ __forceinline__ void walk_sk(const PassArgs& a, int x0, int X, int y0, uint32_t* smem) {
+  constexpr int KS = KM < kVec ? KM : 1;
+  constexpr int NS = 4 + 2 * KS;
+  constexpr bool STRIDE = KM >= kVec;
+  const int k = a.k, N = a.N;
+  const int tid = (int)threadIdx.x;
+  const int nout = min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
+  const int nlist = nout + 2;
+  const bool spans = STRIDE && k >= 256;
+  const int K4 = (k + 3) & ~3;
+  const int SE = stage_elems_sk(k);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
+
+  if (tid < nlist) mbar_init(&bars[tid], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  {  // staging: warp w issues the copies of rows w, w + 4, ... (one elected lane)
+    const int warp = __shfl_sync(0xFFFFFFFFu, tid >> 5, 0);
+    const int P = (int)a.pitch;
+    const int base = x0 - K4;
+    const int lo = max(base, 0), hi = min(x0 + kW + K4, P);
+    int nsp = 0;
+    if (spans)
+      for (int j = -1; j <= 4; ++j) nsp += (x0 + j * k >= 0 && x0 + j * k < N);
+    const uint32_t tx = spans ? 512u * (uint32_t)nsp : (uint32_t)(hi - lo) * 4u;
+    for (int i = warp; i < nlist; i += kThreads / 32) {
+      int r = y0 + (i - 1) * k;  // outside the grid: stage the centre row again
+      if (r < 0) r += k;
+      else if (r >= N) r -= k;
+      const uint32_t* src = BANDED ? row_ptr(a, r) : a.in + (int64_t)(r - a.row0) * a.pitch;
+      uint32_t* dst = smem + (size_t)i * SE;
+      if (elect_one()) {
+        mbar_expect_tx(&bars[i], tx);
+        if (!spans) {
+          bulk_g2s(dst + (lo - base), src + lo, (uint32_t)(hi - lo) * 4u, &bars[i]);
+        } else {
+#pragma unroll 1
+          for (int j = -1; j <= 4; ++j) {
+            const int cs = x0 + j * k;
+            if (cs >= 0 && cs < N) bulk_g2s(dst + (j + 1) * 128, src + cs, 512u, &bars[i]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  // per-thread slot offsets in a stage, columns, and edge flags
+  const uint32_t sh16 = a.sh16;
+  int xs_home[NS], xs_out[kVec];
+  constexpr uint32_t P1 = PACK ? 1u : 0u;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int col = STRIDE ? X + (s - 1) * k : X + s - KS;
+    xs_home[s] = (int)(P1 - ((uint32_t)col << 16));
+  }
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) xs_out[e] = (int)(P1 - ((uint32_t)(STRIDE ? X + e * k : X + e) << 16));
+  const bool left_out = FIX && (STRIDE ? X - k < 0 : X - KS < 0);
+  const bool right_out = FIX && (STRIDE ? X + 4 * k >= N : X + 3 + KS >= N);
+  int xb[kVec];
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) xb[e] = (STRIDE ? X + e * k : X + e) - 128;
+  // kk constants (uniform): exact (k^2, 2k); packed (k^2 2^16 - k, k^2 2^16 + k, 2k 2^16)
+  const uint32_t uk = (uint32_t)k;
+  const uint32_t k2 = PACK ? uk * uk * 65536u - uk : uk * uk;
+  const uint32_t m1 = PACK ? uk * uk * 65536u + uk : 2u * uk;
+  const uint32_t m3 = 2u * uk * 65536u;
+  const int sbase = STRIDE ? (spans ? tid : (X - x0) + K4 - k) : 4 * tid;  // stage index of slot 0's vector / label
+
+  uint32_t loc_acc = 0;
+  bool loc_bad = false;
+  using R_t = RowS<NS>;
+  auto consume = [&](int i, R_t& R) {
+    mbar_wait(&bars[i], 0u);
+    const uint32_t* st = smem + (size_t)i * SE;
+    uint32_t lab[NS];
+    if constexpr (!STRIDE) {
+      uint32_t w[12];
+      unpack(*reinterpret_cast<const uint4*>(st + sbase), w);
+      unpack(*reinterpret_cast<const uint4*>(st + sbase + 4), w + 4);
+      unpack(*reinterpret_cast<const uint4*>(st + sbase + 8), w + 8);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) lab[s] = w[s - KS + 4];
+    } else {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) lab[s] = st[sbase + s * (spans ? 128 : k)];
+    }
+    if constexpr (FIX) {  // out-of-grid neighbour -> the same output's centre label (a duplicate)
+#pragma unroll
+      for (int s = 0; s < KS; ++s) lab[s] = left_out ? lab[s + KS] : lab[s];
+#pragma unroll
+      for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
+    }
+    build_sk<KS, MAY_EMPTY, PACK>(lab, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, R);
+  };
+
+  R_t r0, r1, r2;
+  consume(0, r0);
+  consume(1, r1);
+  int y = y0;
+  uint32_t* po = a.out + (int64_t)(y0 - a.row0) * a.pitch + X;
+  const int64_t kp = (int64_t)k * a.pitch;
+  int j = 0;
+  auto step = [&](const R_t& Pv, const R_t& Cv, R_t& Nx) -> bool {
+    consume(j + 2, Nx);
+    uint32_t o[kVec];
+    if constexpr (PACK) {
+      const uint32_t uy = (uint32_t)y;
+      const uint32_t My = 256u - (uy << 17);
+      const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
+      const uint32_t Yb = (uy - 128u) << 16;
+      uint32_t sk[kVec];
+      if (0u - Cy <= 0x80000000u) {
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) sk[e] = min9_sk<false, KS>(Pv, Cv, Nx, e, My) + Cy;
+      } else {
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) sk[e] = min9_sk<true, KS>(Pv, Cv, Nx, e, My) + Cy;
+      }
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) o[e] = __byte_perm(sk[e], 0u, 0x4140) + Yb + (uint32_t)xb[e];
+      loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
+    } else {
+      int mm = -0x7FFFFFFF - 1;
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) {
+        int me;
+        uint32_t v = best_sk<KS>(Pv, Cv, Nx, e, y, me);
+        mm = max(mm, me);
+        if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
+        o[e] = v;
+      }
+      loc_bad |= mm > (int)kLocD2 - y * y;
+    }
+    if constexpr (!STRIDE) {
+      store_out(a, BANDED, y, X, po, make_uint4(o[0], o[1], o[2], o[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) store_out(a, BANDED, y, X + e * k, po + e * k, o[e]);
+    }
+    po += kp;
+    y += k;
+    return ++j < nout;
+  };
+#pragma unroll 1
+  while (true) {
+    if (!step(r0, r1, r2)) break;
+    if (!step(r1, r2, r0)) break;
+    if (!step(r2, r0, r1)) break;
+  }
+  if (a.loc_out) {
+    bool far;
+    if constexpr (PACK) far = loc_acc >= ((kLocD2 + 1u) << 16);
+    else far = loc_bad;
+    if (__syncthreads_or(far) && tid == 0) atomicOr(a.loc_out, 1u);
+  }
+}
+
+// grid (xblocks, segs, residues) as jump_pass_fast.  Host: N % 512 == 0, k a power of two,
+// k in {1, 2} or 32 <= k <= N / 4; Euclidean Moore passes, no window (N <= 32768).
+template <int KM, bool MAY_EMPTY, bool BANDED>
+__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs a) {
+  extern __shared__ __align__(128) uint32_t dyn_smem[];
+  const int xb = (int)blockIdx.x, seg = (int)blockIdx.y, res = (int)blockIdx.z;
+  const int y0 = a.y_lo + res + seg * a.walk * a.k;
+  if (res >= a.k || y0 >= a.y_hi) return;
+  const int k = a.k, tid = (int)threadIdx.x;
+  int x0, X;
+  bool fix;
+  if constexpr (KM < kVec) {
+    x0 = xb * kW;
+    X = x0 + kVec * tid;
+    fix = x0 == 0 || x0 + kW >= a.N;
+  } else if (k <= 128) {
+    x0 = xb * kW;
+    X = x0 + 4 * k * (tid >> a.lk) + (tid & (k - 1));
+    fix = x0 == 0 || x0 + kW >= a.N;
+  } else {
+    const int lr = a.lk - 7;  // k / 128 residue blocks per group of 4k columns
+    const int g = xb >> lr, rb = xb & ((1 << lr) - 1);
+    x0 = 4 * k * g + 128 * rb;
+    X = x0 + tid;
+    fix = g == 0 || x0 - 128 * rb + 4 * k >= a.N;
+  }
+  if constexpr (!MAY_EMPTY) {
+    if (a.loc_in && k <= kPackMaxK && *(volatile const uint32_t*)a.loc_in == 0u) {
+      if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, true>(a, x0, X, y0, dyn_smem);
+      else walk_sk<KM, MAY_EMPTY, BANDED, false, true>(a, x0, X, y0, dyn_smem);
+      return;
+    }
+  }
+  if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false>(a, x0, X, y0, dyn_smem);
+  else walk_sk<KM, MAY_EMPTY, BANDED, false, false>(a, x0, X, y0, dyn_smem);
+}
+
 // ------------------------------------------------------------------ wide jump pass
 //
 // Same pass for what the fast kernels do not take: steps that are not powers of two, steps
