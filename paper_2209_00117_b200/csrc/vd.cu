@@ -6,9 +6,12 @@
 // at run time with dlopen (the library itself does not link NCCL).
 //
 // "P:n" = line n of the paper's LaTeX source; "R-n" = reading n in DESIGN.md §3.
+#include <cuda.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (fetched with cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: ranges per frame and per pass (no-ops unless a tool attaches)
 
 #include <algorithm>
 #include <atomic>
@@ -68,6 +71,13 @@ bool nccl_load() {
   g_nccl.ok = true;
   return true;
 }
+
+// NVTX range for the lifetime of a scope: "vd_jfa", "vd_djfa_step", "pass k=..." (profilers
+// such as nsys / ncu --nvtx show the host-side enqueue structure of a frame).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ schedules (host)
 uint32_t ceil_log2_u64(uint64_t n) {
@@ -424,13 +434,44 @@ cudaError_t launch_fast_k(int dev, bool me, bool bd, bool rel, int metric, bool 
 // Shared-term kernel (jump_pass_sk): one band or banded, Euclidean Moore, N % 512 == 0, and
 // k in {1, 2} (adjacent columns) or 32 <= k <= N/4 (stride columns).  VD_NO_SK=1 disables it
 // (A/B timing).
+// VD_SK_MASK (hex bitmask over log2 k) selects the steps it takes, for A/B timing.
 bool sk_ok(const vd_ctx* h, uint32_t k, bool vn, bool rel) {
   static const bool off = [] { const char* e = getenv("VD_NO_SK"); return e && e[0] == '1'; }();
-  return !off && !rel && !vn && h->metric == 0 && h->N % 512 == 0 && (k <= 2 || (k >= 32 && 4 * k <= h->N));
+  static const uint64_t mask = [] { const char* e = getenv("VD_SK_MASK"); return e ? strtoull(e, nullptr, 16) : ~0ull; }();
+  uint32_t lk = 0;
+  while ((1u << lk) < k) ++lk;
+  return !off && ((mask >> lk) & 1) && !rel && !vn && h->metric == 0 && h->N % 512 == 0 && 4 * k <= h->N;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (libvd does not link libcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// Tensor map of one band's input viewed as [rows][N/k][k] (uint32), box {128, 6, 1}: one copy
+// stages the six 128-column spans x0 + j k (j = -1..4) of a row (jump_pass_sk, k >= 256).
+bool encode_span_map(const vd_ctx* h, const uint32_t* in, uint32_t rows, uint32_t k, CUtensorMap* tm) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {k, h->N / k, rows};
+  const cuuint64_t strides[2] = {(cuuint64_t)k * 4, (cuuint64_t)h->pitch * 4};
+  const cuuint32_t box[3] = {128, 6, 1}, es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(in), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int KM, bool ME, bool BD>
-cudaError_t launch_sk(int dev, const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
+cudaError_t launch_sk(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk, size_t sm,
+                      cudaStream_t st) {
   static std::atomic<uint64_t> opted{0};
   const uint64_t bit = 1ull << (dev & 63);
   if (!(opted.load(std::memory_order_acquire) & bit)) {
@@ -439,13 +480,14 @@ cudaError_t launch_sk(int dev, const vdk::PassArgs& a, dim3 grid, dim3 blk, size
     if (e != cudaSuccess) return e;
     opted.fetch_or(bit, std::memory_order_release);
   }
-  vdk::jump_pass_sk<KM, ME, BD><<<grid, blk, sm, st>>>(a);
+  vdk::jump_pass_sk<KM, ME, BD><<<grid, blk, sm, st>>>(a, tm);
   return cudaSuccess;
 }
 template <int KM>
-cudaError_t launch_sk_k(int dev, bool me, bool bd, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
-  if (me) return bd ? launch_sk<KM, true, true>(dev, a, g, b, sm, st) : launch_sk<KM, true, false>(dev, a, g, b, sm, st);
-  return bd ? launch_sk<KM, false, true>(dev, a, g, b, sm, st) : launch_sk<KM, false, false>(dev, a, g, b, sm, st);
+cudaError_t launch_sk_k(int dev, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 g, dim3 b,
+                        size_t sm, cudaStream_t st) {
+  if (me) return bd ? launch_sk<KM, true, true>(dev, a, tm, g, b, sm, st) : launch_sk<KM, true, false>(dev, a, tm, g, b, sm, st);
+  return bd ? launch_sk<KM, false, true>(dev, a, tm, g, b, sm, st) : launch_sk<KM, false, false>(dev, a, tm, g, b, sm, st);
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
@@ -464,6 +506,9 @@ struct Push {  // where a launch also stores the rows the neighbours' next pass 
 vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn, int64_t y_lo = -1,
                       int64_t y_hi = -1, const Push* push = nullptr) {
   vdk::PassArgs a;
+  a.res_in_y = 0;
+  a.nwalk = 0;
+  a.tmap = 0;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
   a.top = sh.top[h->hpar];
@@ -517,8 +562,30 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     a.segs = (int)((per_res + a.walk - 1) / a.walk);
     a.lk = 0;
     while ((1u << a.lk) < k) ++a.lk;
-    const dim3 grid((unsigned)a.xblocks, (unsigned)a.segs, nres), blk(vdk::kThreads);
+    // Grid order (VD_ORDER, experiment): 0 = residue slowest, 1 = segment slowest
+    static const int order = [] { const char* e = getenv("VD_ORDER"); return e ? atoi(e) : 0; }();
+    a.res_in_y = order == 1 ? 1 : 0;
+    // Whole residue classes per CTA (jump_pass_sk FULL walks) when one class fits the stage: a
+    // one-band pass over the whole grid with k >= N / (walk + 2) (JFA's large steps).
+    // VD_NO_FULL=1 disables it (A/B).
+    static const bool no_full = [] { const char* e = getenv("VD_NO_FULL"); return e && e[0] == '1'; }();
     const bool banded = sh.top[0] != nullptr;
+    a.nwalk = 0;
+    unsigned gz = a.res_in_y ? (unsigned)a.segs : nres, gy = a.res_in_y ? nres : (unsigned)a.segs;
+    if (sk && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
+      const uint32_t per = h->N / k, fit = (uint32_t)vdk::walk_len_sk((int)k) + 2;
+      if (2 * per <= fit) {  // (one class per CTA measured no faster than segment walks)
+        // as many classes per CTA as fit, but keep >= 4 CTAs per SM in the grid
+        const int64_t cap = std::max<int64_t>(1, (int64_t)a.xblocks * k / ((int64_t)h->num_sms * 4));
+        a.nwalk = (int)std::min<int64_t>(fit / per, cap);
+        a.walk = vdk::walk_len_sk((int)k);
+        a.segs = 1;
+        a.res_in_y = 0;
+        gy = 1;
+        gz = (k + (uint32_t)a.nwalk - 1) / (uint32_t)a.nwalk;
+      }
+    }
+    const dim3 grid((unsigned)a.xblocks, gy, gz), blk(vdk::kThreads);
     // locality (the kernels' LOC variants: Euclidean Moore).  A launch whose rows read halo
     // rows (written by other bands, whose locality this band's flag does not cover) keeps
     // the exact walk; the interior launch of an overlapped sharded pass reads none.
@@ -533,18 +600,33 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     const size_t sm = sk ? vdk::pass_smem_sk((int)k) : vdk::pass_smem((int)k, rel);
     cudaError_t e;
     if (sk) {
-      if (k == 1) e = launch_sk_k<1>(h->device, may_empty, banded, a, grid, blk, sm, h->stream);
-      else if (k == 2) e = launch_sk_k<2>(h->device, may_empty, banded, a, grid, blk, sm, h->stream);
-      else e = launch_sk_k<4>(h->device, may_empty, banded, a, grid, blk, sm, h->stream);
+      // k >= 256 on one band: one tensor copy per staged row (VD_NO_TMAP=1: six bulk copies)
+      static const bool no_tmap = [] { const char* e = getenv("VD_NO_TMAP"); return e && e[0] == '1'; }();
+      CUtensorMap tm;
+      memset(&tm, 0, sizeof tm);
+      a.tmap = 0;
+      if (k >= 256 && !banded && !no_tmap && encode_span_map(h, a.in, sh.rows, k, &tm)) a.tmap = 1;
+      switch (k) {
+        case 1: e = launch_sk_k<1>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 2: e = launch_sk_k<2>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 4: e = launch_sk_k<4>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 8: e = launch_sk_k<8>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 16: e = launch_sk_k<16>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 32: e = launch_sk_k<32>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 64: e = launch_sk_k<64>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 128: e = launch_sk_k<128>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        default: e = launch_sk_k<256>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+      }
     } else if (k == 1) e = launch_fast_k<1>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     else if (k == 2) e = launch_fast_k<2>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     else e = launch_fast_k<4>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     CK(e);
   } else {
     h->pass_loc_ok = false;  // the wide kernel does not report locality
-    a.segs = 1;
+    const uint32_t nres = std::min(k, R);
+    a.segs = (int)((R + k - 1) / k);  // rows per residue class
     a.walk = 1;
-    const int64_t blocks = (int64_t)a.xblocks * R;
+    const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 g((unsigned)blocks), b(vdk::kThreads);
     const bool v4 = (k % 4) == 0;
     if (h->metric == 0) {
@@ -605,6 +687,9 @@ vd_status exchange_halos(vd_ctx* h, uint32_t k, cudaStream_t st) {
 // processes a flag in the neighbour's memory announces them (peer_signal / peer_wait).
 vd_status run_pass_body(vd_ctx* h, uint32_t k, bool may_empty, bool vn, uint32_t k_next);
 vd_status run_pass(vd_ctx* h, uint32_t k, bool may_empty, bool vn = false, uint32_t k_next = 0) {
+  char name[32];
+  snprintf(name, sizeof name, "pass k=%u", k);
+  NvtxRange range(name);
   loc_pass_begin(h, k);
   const vd_status st = run_pass_body(h, k, may_empty, vn, k_next);
   loc_pass_end(h);
@@ -1015,13 +1100,40 @@ void vd_destroy(vd_handle h) {
   delete h;
 }
 
+namespace {
+// Pass k_1 of a JFA straight from the seeds (jfa_first_pass): fill the band with the
+// unclaimed label, then scatter every seed's offers.  Same result as init + stamp + gather
+// pass; needs no halo exchange (every rank holds every seed).
+vd_status jfa_init_first_pass(vd_ctx* h, uint32_t k1, bool vn) {
+  const uint32_t u = unclaimed_label(h);
+  for (auto& sh : h->shards) {
+    const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
+    vdk::fill_value<<<grid_for(h, n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u);
+    vd_status st = after_launch(h, "fill_value");
+    if (st) return st;
+    vdk::jfa_first_pass<<<grid_for(h, (int64_t)h->s, 256), 256, 0, h->stream>>>(
+        sh.buf[h->cur], h->pitch, (int)sh.row0, (int)sh.rows, (int)h->N, (int)k1, h->seeds, (int64_t)h->s, u,
+        h->metric, vn ? 1 : 0);
+    if ((st = after_launch(h, "jfa_first_pass"))) return st;
+  }
+  ++h->pass_seq;  // keeps the peer-halo sequence numbers counting passes
+  h->hpar ^= 1;
+  h->pushed_k = 0;
+  return VD_OK;
+}
+}  // namespace
+
 vd_status vd_jfa(vd_handle h) {
   CHECK_HANDLE(h);
   DeviceGuard guard(h->device);
+  NvtxRange range("vd_jfa");
   std::vector<uint32_t> ks;
   schedule_jfa(h->N, h->extras, ks);
-  vd_status st = jfa_init(h);
+  // P:68 + pass k_1, fused (VD_NO_FIRST_SCATTER=1: init + stamp + gather pass, for A/B)
+  static const bool no_scatter = [] { const char* e = getenv("VD_NO_FIRST_SCATTER"); return e && e[0] == '1'; }();
+  vd_status st = no_scatter ? jfa_init(h) : jfa_init_first_pass(h, ks[0], h->jfa_vn_waves > 0);
   if (st) return st;
+  const size_t first = no_scatter ? 0 : 1;
   const bool virt = unclaimed_label(h) != VD_EMPTY;
   // Beyond N = 16384 EMPTY is real and the passes run the 64-bit kernel, which reports
   // whether it left any EMPTY (summed over ranks); from the first pass that leaves none on,
@@ -1029,7 +1141,7 @@ vd_status vd_jfa(vd_handle h) {
   bool may_empty = !virt;
   const bool track = may_empty;
   loc_begin(h);  // the passes report locality; once it holds, the rest take the packed-key kernel
-  for (size_t i = 0; i < ks.size(); ++i) {
+  for (size_t i = first; i < ks.size(); ++i) {
     const bool vn = i < h->jfa_vn_waves;
     if (track && may_empty) {
       CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
@@ -1112,6 +1224,7 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   if (!disp_xy) return VD_ERR_ARG;
   if (!h->has_diagram) return fail(h, VD_ERR_STATE, "vd_djfa_step needs a diagram: call vd_jfa first");
   DeviceGuard guard(h->device);
+  NvtxRange range("vd_djfa_step");
   if (!h->fwd) {  // forward map, kept all-EMPTY between steps
     CK(cudaMalloc(&h->fwd, (size_t)h->N * h->N * sizeof(uint32_t)));
     CK(cudaMemsetAsync(h->fwd, 0xFF, (size_t)h->N * h->N * sizeof(uint32_t), h->stream));
@@ -1131,9 +1244,14 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   //    (one band: the remap also reports whether every label is within kLocR of its pixel,
   //    which lets the passes take the packed-key kernel)
   const bool loc = loc_begin(h);
+  static const int remap_kind = [] { const char* e = getenv("VD_REMAP"); return e ? atoi(e) : 1; }();
   for (auto& sh : h->shards) {
-    vdk::remap<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N, h->fwd,
-                                                           (int)sh.row0, loc ? h->loc : nullptr);
+    if (remap_kind == 1)
+      vdk::remap_lanes<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+                                                                     h->fwd, (int)sh.row0, loc ? h->loc : nullptr);
+    else
+      vdk::remap<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
+                                                               h->fwd, (int)sh.row0, loc ? h->loc : nullptr);
     if ((st = after_launch(h, "remap"))) return st;
   }
   h->loc_valid = loc;

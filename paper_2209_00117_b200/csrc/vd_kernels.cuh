@@ -8,6 +8,7 @@
 // every thread moves 4 labels with one 128-bit load / store.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (type only; the map is encoded on the host through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 namespace vdk {
@@ -43,6 +44,9 @@ struct PassArgs {
   int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / walk)
   int32_t walk;     // output rows per walk (walk_len(k))
   int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
+  int32_t res_in_y; // grid order: 0 = (x-block, segment, residue), 1 = (x-block, residue, segment)
+  int32_t nwalk;    // jump_pass_sk: > 0 = whole residue classes, nwalk of them per CTA (FULL walks)
+  int32_t tmap;     // jump_pass_sk, k >= 256, one band: stage each row's six spans with ONE tensor copy
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
@@ -649,7 +653,8 @@ __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLO
   static_assert(!(MAY_EMPTY && REL), "the windowed path takes complete diagrams only");
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   // grid (xblocks, segs, residues): launched x-fastest, then the walk segments of one residue
-  const int xb = (int)blockIdx.x, seg = (int)blockIdx.y, res = (int)blockIdx.z;
+  const int xb = (int)blockIdx.x;
+  const int seg = (int)(a.res_in_y ? blockIdx.z : blockIdx.y), res = (int)(a.res_in_y ? blockIdx.y : blockIdx.z);
   const int x0 = xb * kW;
   const int y0 = a.y_lo + res + seg * a.walk * a.k;
   if (res >= a.k || y0 >= a.y_hi) return;  // uniform over the CTA
@@ -805,23 +810,33 @@ __device__ __forceinline__ uint32_t min9_sk(const RowS<4 + 2 * KS>& A, const Row
                         __vimin3_u32(kk[6], kk[7], kk[8]));
 }
 
-// One CTA walk of the shared-term pass (see walk() for the staging and the walk structure).
-// KM: 1 or 2 (adjacent, KS = k), 4 (stride, k >= 32, KS = 1).
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK>
-__device__ __forceinline__ void walk_sk(const PassArgs& a, int x0, int X, int y0, uint32_t* smem) {
+// One CTA of the shared-term pass (see walk() for the staging and the walk structure).
+// KM: 1 or 2 (adjacent, KS = k), 4 .. 64 (stride with k == KM known at compile time), 128 (stride,
+// any k >= 128).  FULL: the CTA runs a.nwalk whole residue classes (a one-band pass whose classes
+// have at most a.walk rows: JFA's large steps); their neighbour rows outside the grid are not
+// staged at all (the centre row is reused from registers), and the classes' rows are all staged
+// at entry, so one CTA hides the staging latency of several short walks.  Otherwise the CTA
+// runs one walk segment of a.walk rows starting at y0, as jump_pass_fast.
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL>
+__device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
+                                        uint32_t* smem) {
   constexpr int KS = KM < kVec ? KM : 1;
   constexpr int NS = 4 + 2 * KS;
   constexpr bool STRIDE = KM >= kVec;
-  const int k = a.k, N = a.N;
+  constexpr int KC = (STRIDE && KM <= 128) ? KM : 0;  // compile-time step: immediate offsets
+  const int k = KC ? KC : a.k, N = a.N;
   const int tid = (int)threadIdx.x;
-  const int nout = min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
-  const int nlist = nout + 2;
-  const bool spans = STRIDE && k >= 256;
+  // FULL: walks y0 + w (w < nw), each of nout rows; stage slot of (walk w, row j) = w * nout + j.
+  // Else: one walk; stage slot i = logical row i (0 = the row above the first output row).
+  const int nw = FULL ? min(a.nwalk, k - (y0 - a.y_lo)) : 1;
+  const int nout = FULL ? (a.y_hi - y0 + k - 1) >> a.lk : min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
+  const int nlist = FULL ? nw * nout : nout + 2;
+  const bool spans = STRIDE && !KC && k >= 256;
   const int K4 = (k + 3) & ~3;
   const int SE = stage_elems_sk(k);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
 
-  if (tid < nlist) mbar_init(&bars[tid], 1);
+  for (int i = tid; i < nlist; i += kThreads) mbar_init(&bars[i], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   {  // staging: warp w issues the copies of rows w, w + 4, ... (one elected lane)
@@ -832,17 +847,32 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, int x0, int X, int y0
     int nsp = 0;
     if (spans)
       for (int j = -1; j <= 4; ++j) nsp += (x0 + j * k >= 0 && x0 + j * k < N);
-    const uint32_t tx = spans ? 512u * (uint32_t)nsp : (uint32_t)(hi - lo) * 4u;
+    const uint32_t tx = spans ? (!BANDED && a.tmap ? 3072u : 512u * (uint32_t)nsp) : (uint32_t)(hi - lo) * 4u;
     for (int i = warp; i < nlist; i += kThreads / 32) {
-      int r = y0 + (i - 1) * k;  // outside the grid: stage the centre row again
-      if (r < 0) r += k;
-      else if (r >= N) r -= k;
+      int r;
+      if constexpr (FULL) {
+        const int w = i / nout;
+        r = y0 + w + (i - w * nout) * k;
+      } else {
+        r = y0 + (i - 1) * k;  // outside the grid: stage the centre row again
+        if (r < 0) r += k;
+        else if (r >= N) r -= k;
+      }
       const uint32_t* src = BANDED ? row_ptr(a, r) : a.in + (int64_t)(r - a.row0) * a.pitch;
       uint32_t* dst = smem + (size_t)i * SE;
       if (elect_one()) {
         mbar_expect_tx(&bars[i], tx);
         if (!spans) {
           bulk_g2s(dst + (lo - base), src + lo, (uint32_t)(hi - lo) * 4u, &bars[i]);
+        } else if (!BANDED && a.tmap) {
+          // the row as a [N/k][k] array: box {128 columns, 6 blocks} at (x0 mod k, j = g*4 - 1);
+          // blocks outside the grid arrive zero-filled (replaced by the FIX substitution)
+          const int c0 = x0 & (k - 1), c1 = (x0 >> a.lk) - 1;
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+              "[%5];" ::"r"(smem_u32(dst)),
+              "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(r - a.row0), "r"(smem_u32(&bars[i]))
+              : "memory");
         } else {
 #pragma unroll 1
           for (int j = -1; j <= 4; ++j) {
@@ -871,7 +901,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, int x0, int X, int y0
   int xb[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) xb[e] = (STRIDE ? X + e * k : X + e) - 128;
-  // kk constants (uniform): exact (k^2, 2k); packed (k^2 2^16 - k, k^2 2^16 + k, 2k 2^16)
+  // constants (uniform): exact (k^2, 2k); packed (k^2 2^16 - k, k^2 2^16 + k, 2k 2^16)
   const uint32_t uk = (uint32_t)k;
   const uint32_t k2 = PACK ? uk * uk * 65536u - uk : uk * uk;
   const uint32_t m1 = PACK ? uk * uk * 65536u + uk : 2u * uk;
@@ -905,59 +935,76 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, int x0, int X, int y0
     build_sk<KS, MAY_EMPTY, PACK>(lab, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, R);
   };
 
-  R_t r0, r1, r2;
-  consume(0, r0);
-  consume(1, r1);
-  int y = y0;
-  uint32_t* po = a.out + (int64_t)(y0 - a.row0) * a.pitch + X;
   const int64_t kp = (int64_t)k * a.pitch;
-  int j = 0;
-  auto step = [&](const R_t& Pv, const R_t& Cv, R_t& Nx) -> bool {
-    consume(j + 2, Nx);
-    uint32_t o[kVec];
-    if constexpr (PACK) {
-      const uint32_t uy = (uint32_t)y;
-      const uint32_t My = 256u - (uy << 17);
-      const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
-      const uint32_t Yb = (uy - 128u) << 16;
-      uint32_t sk[kVec];
-      if (0u - Cy <= 0x80000000u) {
+  // One walk: output rows yw, yw + k, ... (n rows).  Logical input row i (0 = the row above the
+  // first output, n + 1 = the row below the last) is stage slot ibase + i; FULL walks have no
+  // rows 0 and n + 1 in the stage (outside the grid: the centre row is a duplicate candidate).
+  auto run = [&](int yw, int n, int ibase) {
+    R_t r0, r1, r2;
+    if constexpr (FULL) {
+      consume(ibase + 1, r1);
+      r0 = r1;
+    } else {
+      consume(ibase, r0);
+      consume(ibase + 1, r1);
+    }
+    int y = yw;
+    uint32_t* po = a.out + (int64_t)(yw - a.row0) * a.pitch + X;
+    int j = 0;
+    auto step = [&](const R_t& Pv, const R_t& Cv, R_t& Nx) -> bool {
+      if (!FULL || j + 1 < n) consume(ibase + j + 2, Nx);
+      else Nx = Cv;
+      uint32_t o[kVec];
+      if constexpr (PACK) {
+        const uint32_t uy = (uint32_t)y;
+        const uint32_t My = 256u - (uy << 17);
+        const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
+        const uint32_t Yb = (uy - 128u) << 16;
+        uint32_t sk[kVec];
+        if (0u - Cy <= 0x80000000u) {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) sk[e] = min9_sk<false, KS>(Pv, Cv, Nx, e, My) + Cy;
+          for (int e = 0; e < kVec; ++e) sk[e] = min9_sk<false, KS>(Pv, Cv, Nx, e, My) + Cy;
+        } else {
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) sk[e] = min9_sk<true, KS>(Pv, Cv, Nx, e, My) + Cy;
+        }
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) o[e] = __byte_perm(sk[e], 0u, 0x4140) + Yb + (uint32_t)xb[e];
+        loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
+      } else {
+        int mm = -0x7FFFFFFF - 1;
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          int me;
+          uint32_t v = best_sk<KS>(Pv, Cv, Nx, e, y, me);
+          mm = max(mm, me);
+          if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
+          o[e] = v;
+        }
+        loc_bad |= mm > (int)kLocD2 - y * y;
+      }
+      if constexpr (!STRIDE) {
+        store_out(a, BANDED, y, X, po, make_uint4(o[0], o[1], o[2], o[3]));
       } else {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) sk[e] = min9_sk<true, KS>(Pv, Cv, Nx, e, My) + Cy;
+        for (int e = 0; e < kVec; ++e) store_out(a, BANDED, y, X + e * k, po + e * k, o[e]);
       }
-#pragma unroll
-      for (int e = 0; e < kVec; ++e) o[e] = __byte_perm(sk[e], 0u, 0x4140) + Yb + (uint32_t)xb[e];
-      loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
-    } else {
-      int mm = -0x7FFFFFFF - 1;
-#pragma unroll
-      for (int e = 0; e < kVec; ++e) {
-        int me;
-        uint32_t v = best_sk<KS>(Pv, Cv, Nx, e, y, me);
-        mm = max(mm, me);
-        if (MAY_EMPTY) v = (v == a.vempty) ? EMPTY : v;
-        o[e] = v;
-      }
-      loc_bad |= mm > (int)kLocD2 - y * y;
-    }
-    if constexpr (!STRIDE) {
-      store_out(a, BANDED, y, X, po, make_uint4(o[0], o[1], o[2], o[3]));
-    } else {
-#pragma unroll
-      for (int e = 0; e < kVec; ++e) store_out(a, BANDED, y, X + e * k, po + e * k, o[e]);
-    }
-    po += kp;
-    y += k;
-    return ++j < nout;
-  };
+      po += kp;
+      y += k;
+      return ++j < n;
+    };
 #pragma unroll 1
-  while (true) {
-    if (!step(r0, r1, r2)) break;
-    if (!step(r1, r2, r0)) break;
-    if (!step(r2, r0, r1)) break;
+    while (true) {
+      if (!step(r0, r1, r2)) break;
+      if (!step(r1, r2, r0)) break;
+      if (!step(r2, r0, r1)) break;
+    }
+  };
+  if constexpr (FULL) {
+#pragma unroll 1
+    for (int w = 0; w < nw; ++w) run(y0 + w, nout, w * nout - 1);
+  } else {
+    run(y0, nout, 0);
   }
   if (a.loc_out) {
     bool far;
@@ -967,12 +1014,17 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, int x0, int X, int y0
   }
 }
 
-// grid (xblocks, segs, residues) as jump_pass_fast.  Host: N % 512 == 0, k a power of two,
-// k in {1, 2} or 32 <= k <= N / 4; Euclidean Moore passes, no window (N <= 32768).
+// grid (xblocks, segs, residues) as jump_pass_fast; with a.nwalk > 0 (FULL) the z index counts
+// groups of a.nwalk residue classes.  Host: N % 512 == 0, k a power of two, k <= N / 4;
+// Euclidean Moore passes, no window (N <= 32768).  KM: k itself for k <= 128 (compile-time
+// step), 256 for any larger k.
 template <int KM, bool MAY_EMPTY, bool BANDED>
-__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
-  const int xb = (int)blockIdx.x, seg = (int)blockIdx.y, res = (int)blockIdx.z;
+  const int xb = (int)blockIdx.x;
+  const bool full = a.nwalk > 0;
+  const int seg = full ? 0 : (int)(a.res_in_y ? blockIdx.z : blockIdx.y);
+  const int res = full ? (int)blockIdx.z * a.nwalk : (int)(a.res_in_y ? blockIdx.y : blockIdx.z);
   const int y0 = a.y_lo + res + seg * a.walk * a.k;
   if (res >= a.k || y0 >= a.y_hi) return;
   const int k = a.k, tid = (int)threadIdx.x;
@@ -982,9 +1034,9 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
     x0 = xb * kW;
     X = x0 + kVec * tid;
     fix = x0 == 0 || x0 + kW >= a.N;
-  } else if (k <= 128) {
+  } else if (KM <= 128) {  // k == KM
     x0 = xb * kW;
-    X = x0 + 4 * k * (tid >> a.lk) + (tid & (k - 1));
+    X = x0 + 4 * KM * (tid / KM) + (tid % KM);
     fix = x0 == 0 || x0 + kW >= a.N;
   } else {
     const int lr = a.lk - 7;  // k / 128 residue blocks per group of 4k columns
@@ -993,15 +1045,20 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
     X = x0 + tid;
     fix = g == 0 || x0 - 128 * rb + 4 * k >= a.N;
   }
+  if (full) {  // JFA's large steps: exact walk (their diagrams are never local)
+    if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    else walk_sk<KM, MAY_EMPTY, BANDED, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    return;
+  }
   if constexpr (!MAY_EMPTY) {
     if (a.loc_in && k <= kPackMaxK && *(volatile const uint32_t*)a.loc_in == 0u) {
-      if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, true>(a, x0, X, y0, dyn_smem);
-      else walk_sk<KM, MAY_EMPTY, BANDED, false, true>(a, x0, X, y0, dyn_smem);
+      if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, true, false>(a, &tm, x0, X, y0, dyn_smem);
+      else walk_sk<KM, MAY_EMPTY, BANDED, false, true, false>(a, &tm, x0, X, y0, dyn_smem);
       return;
     }
   }
-  if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false>(a, x0, X, y0, dyn_smem);
-  else walk_sk<KM, MAY_EMPTY, BANDED, false, false>(a, x0, X, y0, dyn_smem);
+  if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, false>(a, &tm, x0, X, y0, dyn_smem);
+  else walk_sk<KM, MAY_EMPTY, BANDED, false, false, false>(a, &tm, x0, X, y0, dyn_smem);
 }
 
 // ------------------------------------------------------------------ wide jump pass
@@ -1012,13 +1069,16 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
 // Generic pass (any k, any N <= 65536, EMPTY allowed): one thread = 4 pixels of one row,
 // 64-bit keys, candidates read straight from global memory (L2-friendly for the large steps
 // it serves).  V4: k % 4 == 0, so the neighbour columns are 16-byte aligned vectors.
+// Rows are launched residue class by residue class (y_lo + r, y_lo + r + k, ... = a.segs rows
+// per class), so that consecutive CTA rows share two of their three input rows in L2.
 template <int METRIC, bool VN, bool V4>
 __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
   const int xb = (int)(blockIdx.x % (unsigned)a.xblocks);
-  const int yl = (int)(blockIdx.x / (unsigned)a.xblocks);
+  const int j = (int)(blockIdx.x / (unsigned)a.xblocks);
+  const int res = j / a.segs, seg = j - res * a.segs;
   const int x = (xb * kThreads + (int)threadIdx.x) * 4;
-  const int y = a.y_lo + yl, k = a.k, N = a.N;
-  const bool live = x < N && y < a.y_hi;
+  const int y = a.y_lo + res + seg * a.k, k = a.k, N = a.N;
+  const bool live = x < N && y < a.y_hi && res < a.k;
   bool any_empty = false;
   if (live) {
     uint32_t best[4];
@@ -1137,6 +1197,43 @@ __global__ void stamp(uint32_t* __restrict__ g, int64_t pitch, int row0, int row
   }
 }
 
+// First JFA pass fused with the initialisation.  The input of pass k_1 is "unclaimed
+// everywhere, each seed pixel holds its seed", so its output at pixel p is the best of
+// the seeds at p and at p + o k_1, o in Table 1: Alg. 1's scatter form of the
+// pass (R-12), where every seed offers itself to the pixels q - o k_1.  The grid
+// (this band) must already hold `unclaimed` everywhere (fill_value).  An offer is a CAS loop
+// on the pixel's label with the exact key (distance in uint64, then label; R-3), so the
+// result is the minimum over all offers in any order -- the gather pass's result.
+// metric 0/1 (Euclidean / Manhattan), vn: Von Neumann offsets only (Table 1's axis ones).
+__device__ __forceinline__ uint64_t dist_c(uint32_t c, int x, int y, int metric) {
+  const uint32_t dx = (uint32_t)abs((int)(c & 0xFFFFu) - x), dy = (uint32_t)abs((int)(c >> 16) - y);
+  return metric == 0 ? (uint64_t)(dx * dx) + (uint64_t)(dy * dy) : (uint64_t)(dx + dy);
+}
+__global__ void jfa_first_pass(uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N, int k,
+                               const uint32_t* __restrict__ seeds, int64_t s, uint32_t unclaimed, int metric, int vn) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = seeds[i];
+    const int cx = (int)(c & 0xFFFFu), cy = (int)(c >> 16);
+#pragma unroll
+    for (int oy = -1; oy <= 1; ++oy) {
+#pragma unroll
+      for (int ox = -1; ox <= 1; ++ox) {
+        if (vn && ox != 0 && oy != 0) continue;
+        const int px = cx - ox * k, py = cy - oy * k;  // the pixel whose neighbour o*k is this seed
+        if (px < 0 || px >= N || py < row0 || py >= row0 + rows || py >= N) continue;
+        uint32_t* a = g + (int64_t)(py - row0) * pitch + px;
+        const uint64_t dc = dist_c(c, px, py, metric);
+        uint32_t cur = *(volatile uint32_t*)a;
+        while (cur == unclaimed || dc < dist_c(cur, px, py, metric) || (dc == dist_c(cur, px, py, metric) && c < cur)) {
+          const uint32_t prev = atomicCAS(a, cur, c);
+          if (prev == cur) break;
+          cur = prev;
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ dJFA
 // SimulateParticles (Alg. 1): new = clamp(old + disp) per axis (R-10); at
 // N = 65536 the EMPTY pixel (65535, 65535) is reserved -> (65534, 65535) (R-4).
@@ -1224,6 +1321,43 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
         }
       }
       *p = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  const bool far = (mx >> 16) > 88u || (mx & 0xFFFFu) > 88u;
+  if (loc && __syncthreads_or(far) && threadIdx.x == 0) atomicOr(loc, 1u);
+}
+
+// The same remap with lanes on consecutive pixels: a warp covers 32 consecutive pixels per
+// access (four such groups per thread and round), so one gather instruction of the warp
+// touches the fwd entries of the 2-3 seeds whose regions cross those 32 pixels instead of
+// the 8-10 seeds of a 128-pixel span (fewer L1 wavefronts per gather).  Same result and the
+// same locality flag as remap().
+__global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd,
+                            int row0, uint32_t* __restrict__ loc) {
+  uint32_t mx = 0;
+  const int lane = (int)threadIdx.x & 31, warp = (int)threadIdx.x >> 5, nwarps = (int)blockDim.x >> 5;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    uint32_t* row = g + (int64_t)r * pitch;
+    const uint32_t nb = __vsub2(0x002C002Cu, ((uint32_t)(row0 + r) << 16));  // (44 - y, 44) per lane
+#pragma unroll 2
+    for (int x0 = 128 * warp; x0 < N; x0 += 128 * nwarps) {
+      uint32_t c[4], nc[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int x = x0 + 32 * e + lane;
+        c[e] = x < N ? row[x] : EMPTY;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        nc[e] = c[e] != EMPTY ? __ldg(fwd + (int64_t)(c[e] >> 16) * N + (c[e] & 0xFFFFu)) : EMPTY;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int x = x0 + 32 * e + lane;
+        if (x < N) {
+          row[x] = nc[e];
+          mx = __vmaxu2(mx, nc[e] == EMPTY ? 0xFFFFFFFFu : __vadd2(nc[e], __vsub2(nb, (uint32_t)x)));
+        }
+      }
     }
   }
   const bool far = (mx >> 16) > 88u || (mx & 0xFFFFu) > 88u;

@@ -43,6 +43,7 @@ ncuremap) timeout 900 ncu --set full --clock-control none --import-source on -k 
 c5launch) VD_CFG=C5 VD_FRAMES=2 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c5_launches_$TAG.csv python scripts/profile_pass.py > gpurun_out/c5_launches_$TAG.log 2>&1 ;;
 variants) timeout 1500 python scripts/time_variants.py 2>&1 | tee gpurun_out/variants_$TAG.txt ;;
 skab) timeout 900 python scripts/time_variants.py VD_NO_SK=1,0 2>&1 | tee gpurun_out/skab_$TAG.txt ;;
+envab) timeout 900 python scripts/time_variants.py $ENVAB 2>&1 | tee -a gpurun_out/envab_$TAG.txt ;;
 sanitize) for tool in memcheck racecheck synccheck initcheck; do
     echo "# compute-sanitizer --tool $tool python scripts/sanitize_small.py ($TAG)" > gpurun_out/sanitizer_${tool}_$TAG.txt
     timeout 1200 compute-sanitizer --tool $tool python scripts/sanitize_small.py >> gpurun_out/sanitizer_${tool}_$TAG.txt 2>&1

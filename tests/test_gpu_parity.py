@@ -54,11 +54,13 @@ def test_jfa_extras_bit_exact(vd, extras):
     assert np.array_equal(d.labels(), oracle.jfa(N, xy, extras))
 
 
-@pytest.mark.parametrize("N", [2, 3, 5, 8, 13, 64, 100, 257, 1024, 1031, 2051])
+@pytest.mark.parametrize("N", [2, 3, 5, 8, 13, 64, 100, 257, 1024, 1031, 2048, 2051])
 def test_single_pass_random_states_bit_exact(vd, N):
     # One pass from arbitrary label maps (seeds and EMPTY mixed, not only reachable
     # states), for every k regime: 1, 2, multiples of 4, >= 512 and non-powers of two
-    # (generic kernel).
+    # (generic kernel).  N = 1024 / 2048: the shared-term kernel (jump_pass_sk) at every step
+    # it takes -- adjacent (k <= 2), compile-time stride (4 .. 128), staged spans (>= 256) and
+    # whole residue classes per CTA (N/k rows fit the stage).
     rng = np.random.default_rng(N)
     s = min(N * N, 40)
     xy = synth.uniform_seeds(N, s, rng_seed=N)
@@ -66,7 +68,7 @@ def test_single_pass_random_states_bit_exact(vd, N):
     d = vd.VoronoiDiagram(N, xy)
     for trial in range(3):
         G = labels[rng.integers(0, len(labels), size=(N, N))]
-        for k in sorted({1, 2, 3, 4, 5, 8, 16, 64, 512, 1024} | {max(1, N // 2)}):
+        for k in sorted({1, 2, 3, 4, 5, 8, 16, 32, 64, 128, 256, 512, 1024} | {max(1, N // 2)}):
             d.set_labels(G)
             d.jump_pass(k)
             assert np.array_equal(d.labels(), oracle.jump_pass(G, k)), (trial, k)
@@ -660,6 +662,31 @@ def test_packed_passes_ragged_grid_bit_exact(vd, N):
     # N not a multiple of 512 (edge CTAs) / of 4 (partial vectors)
     d, packed = _djfa_frames_packed(vd, N, N * N // 256, 1, 3, N)
     assert max(packed) > 0
+
+
+@pytest.mark.parametrize("env", ["VD_NO_FIRST_SCATTER=1", "VD_NO_SK=1", "VD_NO_FULL=1", "VD_ORDER=1", "VD_REMAP=0"])
+def test_kernel_variant_switches_bit_exact(vd, env):
+    # The A/B switches (read once per process) select the r01 kernels: JFA's init + gather
+    # first pass instead of the seed scatter, jump_pass_fast instead of jump_pass_sk, segment
+    # walks instead of whole residue classes, the other grid order, the quad-per-thread remap.
+    # Same labels either way.
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, synth, oracle, paper_2209_00117_b200 as vd\n"
+        "for N, s, G in ((1024, 4096, 0), (2048, 300, 0), (1024, 1024, 4)):\n"
+        "    xy = synth.uniform_seeds(N, s, rng_seed=N + s)\n"
+        "    d = vd.VoronoiDiagram(N, xy, virtual_shards=G); d.jfa(); ref = oracle.jfa(N, xy)\n"
+        "    assert np.array_equal(d.labels(), ref), (N, s, G)\n"
+        "    for f in range(2):\n"
+        "        disp = synth.displacements(s, 2, f, rng_seed=N)\n"
+        "        d.djfa_step(disp, 2); ref, xy, _ = oracle.djfa_step(N, xy, disp, 2, ref)\n"
+        "        assert np.array_equal(d.labels(), ref), (N, s, G, f)\n"
+    )
+    name, val = env.split("=")
+    e = dict(os.environ, **{name: val})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=e, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
 
 
 def test_packed_passes_disabled_env(vd, tmp_path):
