@@ -215,13 +215,14 @@ vd_status vd_last_packed_passes(vd_handle h, uint32_t* passes);
 vd_status vd_synchronize(vd_handle h);
 
 /* Instrumentation: when enabled, CUDA events are recorded around every jump-pass launch
- * on the handle's stream; vd_pass_timing returns the summed device time (ms), the number
- * of timed launches and the pixels they covered, then resets the accumulators. */
+ * on the handle's stream; vd_pass_timing returns the summed device time (ms) of the jump
+ * passes, their number and the pixels they covered, then resets the accumulators. */
 vd_status vd_set_pass_timing(vd_handle h, int enable);
 vd_status vd_pass_timing(vd_handle h, double* ms, uint64_t* launches, uint64_t* pixels);
 /* The timed intervals accumulated since the last vd_pass_timing, one per jump pass (all of
  * its launches): device time ms[i] and step ks[i], for i < min(*n, cap); *n = how many
- * there are.  Does not reset (vd_pass_timing does).  ms / ks may be NULL. */
+ * there are.  A vd_djfa_step's remap is also an interval, with ks[i] = 0 (it covers no
+ * pass pixels).  Does not reset (vd_pass_timing does).  ms / ks may be NULL. */
 vd_status vd_pass_times(vd_handle h, float* ms, uint32_t* ks, uint32_t cap, uint32_t* n);
 
 /* Number of kernels this handle has launched since creation. */

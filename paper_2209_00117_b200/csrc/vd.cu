@@ -124,7 +124,8 @@ void halo_plan(uint32_t N, uint32_t world, uint32_t rank, uint32_t k, vd_halo_pl
   p.send_bot_row0 = B - h;
 }
 
-constexpr uint32_t kLocSlots = 64;  // locality flags per frame (>= passes + 1)
+constexpr uint32_t kLocSlots = 64;  // locality flags per frame (>= passes + 2)
+constexpr uint32_t kLocPrev = kLocSlots - 1;  // persistent: the current diagram's flag (0 = every label local)
 
 struct Shard {
   uint32_t row0 = 0, rows = 0;
@@ -178,6 +179,8 @@ struct vd_ctx {
   uint32_t* pass_loc_out = nullptr;       // ... and output flag (null: not tracked)
   bool pass_loc_ok = false;               // every launch of the pass reported into pass_loc_out
   bool pass_loc_used = false;             // some launch of the pass could take the packed walk
+  bool fuse_remap = false;                // the next pass remaps its staged rows (NEXT-1, jump_pass_sk_remap)
+  bool fuse_pack = false;                 // ... and may take the packed walk (previous flag + move bound)
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -217,10 +220,13 @@ bool loc_begin(vd_ctx* h) {
   h->loc_idx = 0;
   h->loc_valid = false;
   h->loc_passes.clear();
-  if (h->loc_on && cudaMemsetAsync(h->loc, 0, kLocSlots * sizeof(uint32_t), h->stream) != cudaSuccess)
+  if (h->loc_on && cudaMemsetAsync(h->loc, 0, kLocPrev * sizeof(uint32_t), h->stream) != cudaSuccess)
     h->loc_on = false;
   return h->loc_on;
 }
+// The diagram changed outside a tracked frame (set_labels, a single pass, StF): its locality is
+// unknown, which reads as "not local".
+void loc_forget(vd_ctx* h) { cudaMemsetAsync(h->loc + kLocPrev, 0x01, sizeof(uint32_t), h->stream); }
 // One pass: its input flag is the previous pass's output flag; all of its launches (one per
 // shard, or interior + edge strips) OR into one output slot.
 void loc_pass_begin(vd_ctx* h, uint32_t k) {
@@ -228,11 +234,13 @@ void loc_pass_begin(vd_ctx* h, uint32_t k) {
   h->pass_loc_out = nullptr;
   h->pass_loc_ok = false;
   h->pass_loc_used = false;
-  if (!h->loc_on || h->loc_idx + 1 >= kLocSlots) return;
-  h->pass_loc_in = h->loc_valid ? h->loc + h->loc_idx : nullptr;
+  if (!h->loc_on || h->loc_idx + 2 >= kLocSlots) return;
+  int32_t in_slot = h->loc_valid ? (int32_t)h->loc_idx : -1;
+  if (h->fuse_remap) in_slot = h->fuse_pack ? (int32_t)kLocPrev : -1;  // the previous frame's flag
+  h->pass_loc_in = in_slot >= 0 ? h->loc + in_slot : nullptr;
   h->pass_loc_out = h->loc + h->loc_idx + 1;
   h->pass_loc_ok = true;
-  h->loc_passes.emplace_back(h->loc_valid ? (int32_t)h->loc_idx : -1, k);
+  h->loc_passes.emplace_back(in_slot, k);
 }
 void loc_pass_end(vd_ctx* h) {
   if (h->pass_loc_out && !h->pass_loc_used) h->loc_passes.back().first = -1;  // no launch could pack
@@ -242,6 +250,11 @@ void loc_pass_end(vd_ctx* h) {
   h->pass_loc_out = nullptr;
 }
 void loc_end(vd_ctx* h) {
+  // keep the frame's final flag for the next frame's fused first pass
+  if (h->loc_on && h->loc_valid)
+    cudaMemcpyAsync(h->loc + kLocPrev, h->loc + h->loc_idx, sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream);
+  else
+    loc_forget(h);
   h->loc_on = h->loc_valid = false;
   h->loc_last.swap(h->loc_passes);
   h->loc_passes.clear();
@@ -484,6 +497,21 @@ cudaError_t launch_sk(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, di
   return cudaSuccess;
 }
 template <int KM>
+cudaError_t launch_sk_remap(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk, size_t sm,
+                            cudaStream_t st) {
+  static std::atomic<uint64_t> opted{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(opted.load(std::memory_order_acquire) & bit)) {
+    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk_remap<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               vdk::kSmemBudget);
+    if (e != cudaSuccess) return e;
+    opted.fetch_or(bit, std::memory_order_release);
+  }
+  vdk::jump_pass_sk_remap<KM><<<grid, blk, sm, st>>>(a, tm);
+  return cudaSuccess;
+}
+
+template <int KM>
 cudaError_t launch_sk_k(int dev, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 g, dim3 b,
                         size_t sm, cudaStream_t st) {
   if (me) return bd ? launch_sk<KM, true, true>(dev, a, tm, g, b, sm, st) : launch_sk<KM, true, false>(dev, a, tm, g, b, sm, st);
@@ -509,6 +537,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.res_in_y = 0;
   a.nwalk = 0;
   a.tmap = 0;
+  a.fwd = nullptr;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
   a.top = sh.top[h->hpar];
@@ -564,7 +593,10 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     while ((1u << a.lk) < k) ++a.lk;
     // Grid order (VD_ORDER, experiment): 0 = residue slowest, 1 = segment slowest
     static const int order = [] { const char* e = getenv("VD_ORDER"); return e ? atoi(e) : 0; }();
-    a.res_in_y = order == 1 ? 1 : 0;
+    // the fused remap pass defaults to segment-slowest order: concurrent CTAs then cover a band
+    // of rows, whose seeds' fwd entries stay in L2 (VD_FUSE_ORDER=0: residue slowest)
+    static const int fuse_order = [] { const char* e = getenv("VD_FUSE_ORDER"); return e ? atoi(e) : 1; }();
+    a.res_in_y = (h->fuse_remap ? fuse_order : order) == 1 ? 1 : 0;
     // Whole residue classes per CTA (jump_pass_sk FULL walks) when one class fits the stage: a
     // one-band pass over the whole grid with k >= N / (walk + 2) (JFA's large steps).
     // VD_NO_FULL=1 disables it (A/B).
@@ -572,7 +604,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     const bool banded = sh.top[0] != nullptr;
     a.nwalk = 0;
     unsigned gz = a.res_in_y ? (unsigned)a.segs : nres, gy = a.res_in_y ? nres : (unsigned)a.segs;
-    if (sk && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
+    if (sk && !h->fuse_remap && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
       const uint32_t per = h->N / k, fit = (uint32_t)vdk::walk_len_sk((int)k) + 2;
       if (2 * per <= fit) {  // (one class per CTA measured no faster than segment walks)
         // as many classes per CTA as fit, but keep >= 4 CTAs per SM in the grid
@@ -606,6 +638,20 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
       memset(&tm, 0, sizeof tm);
       a.tmap = 0;
       if (k >= 256 && !banded && !no_tmap && encode_span_map(h, a.in, sh.rows, k, &tm)) a.tmap = 1;
+      if (h->fuse_remap) {  // first dJFA pass with the remap fused in (vd_djfa_step checked the conditions)
+        a.fwd = h->fwd;
+        a.loc_in = h->pass_loc_in;  // the previous frame's locality, when the moves keep the packed key valid
+        a.nwalk = 0;
+        const dim3 g2((unsigned)a.xblocks, a.res_in_y ? nres : (unsigned)a.segs, a.res_in_y ? (unsigned)a.segs : nres);
+        switch (k) {
+          case 4: e = launch_sk_remap<4>(h->device, a, tm, g2, blk, sm, h->stream); break;
+          case 8: e = launch_sk_remap<8>(h->device, a, tm, g2, blk, sm, h->stream); break;
+          case 16: e = launch_sk_remap<16>(h->device, a, tm, g2, blk, sm, h->stream); break;
+          case 32: e = launch_sk_remap<32>(h->device, a, tm, g2, blk, sm, h->stream); break;
+          case 64: e = launch_sk_remap<64>(h->device, a, tm, g2, blk, sm, h->stream); break;
+          default: e = launch_sk_remap<128>(h->device, a, tm, g2, blk, sm, h->stream); break;
+        }
+      } else
       switch (k) {
         case 1: e = launch_sk_k<1>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 2: e = launch_sk_k<2>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
@@ -615,7 +661,12 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
         case 32: e = launch_sk_k<32>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 64: e = launch_sk_k<64>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 128: e = launch_sk_k<128>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        default: e = launch_sk_k<256>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 256: e = launch_sk_k<256>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 512: e = launch_sk_k<512>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 1024: e = launch_sk_k<1024>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 2048: e = launch_sk_k<2048>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 4096: e = launch_sk_k<4096>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        default: e = launch_sk_k<8192>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
       }
     } else if (k == 1) e = launch_fast_k<1>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
     else if (k == 2) e = launch_fast_k<2>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
@@ -1072,6 +1123,7 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   }
   CKC(cudaMalloc(&h->counter, sizeof(unsigned long long)));
   CKC(cudaMalloc(&h->loc, kLocSlots * sizeof(uint32_t)));
+  CKC(cudaMemsetAsync(h->loc, 0x01, kLocSlots * sizeof(uint32_t), h->stream));  // nothing known to be local
   CKC(cudaMalloc(&h->flags, 2 * sizeof(uint32_t)));
   CKC(cudaMemset(h->flags, 0, 2 * sizeof(uint32_t)));
   CKC(cudaHostAlloc(&h->peer_err_h, sizeof(uint32_t), cudaHostAllocMapped));
@@ -1204,6 +1256,7 @@ vd_status vd_stf(vd_handle h, uint32_t* passes) {
   }
   h->last_passes = n;
   h->has_diagram = true;
+  loc_forget(h);
   if (passes) *passes = n;
   return VD_OK;
 }
@@ -1240,11 +1293,43 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N);
   if ((st = after_launch(h, "move_fwd"))) return st;
   CK(cudaEventRecord(h->disp_used[slot], h->stream));
+  const bool loc = loc_begin(h);
+  // NEXT-1: on one band the first pass remaps its own staged rows (jump_pass_sk_remap): the
+  // new seed pixels are re-stamped first (flagged), the remapped diagram never goes to HBM,
+  // and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
+  static const bool no_fuse = [] { const char* e = getenv("VD_NO_FUSE"); return e && e[0] == '1'; }();
+  const uint32_t k1 = ks[0];
+  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->N <= 32768 &&
+                    !h->force_rel && sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
+  if (fuse) {
+    Shard& sh = h->shards[0];
+    vdk::stamp_flagged<<<gs, 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0, (int)sh.rows, h->seeds_new,
+                                                  (int64_t)h->s);
+    if ((st = after_launch(h, "stamp_flagged"))) return st;
+    // Packed walk for the fused pass: every label of the previous diagram within kLocR of its
+    // pixel (its flag, kLocPrev) and seeds that moved at most d_max per axis leave every remapped
+    // label within kLocR + d_max*sqrt(2) of its pixel, so a candidate is within that + k1 per
+    // axis; the packed key needs <= 127.  Otherwise the exact walk.
+    const bool pack_ok = k1 <= (uint32_t)vdk::kPackMaxK && (uint64_t)vdk::kLocR + (3ull * d_max + 1) / 2 + k1 <= 127;
+    h->fuse_pack = pack_ok;
+    h->fuse_remap = true;
+    st = run_pass(h, k1, false, false, ks.size() > 1 ? ks[1] : 0);
+    h->fuse_remap = false;
+    if (st) return loc_end(h), st;
+    vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, (int64_t)h->s);
+    if ((st = after_launch(h, "fwd_reset"))) return st;
+    std::swap(h->seeds, h->seeds_new);
+    for (size_t i = 1; i < ks.size(); ++i)
+      if ((st = run_pass(h, ks[i], false, false, i + 1 < ks.size() ? ks[i + 1] : 0))) return loc_end(h), st;
+    loc_end(h);
+    h->last_passes = (uint32_t)ks.size();
+    return VD_OK;
+  }
   // 2. labels follow their seeds (reuse of VD_{t-1})
   //    (one band: the remap also reports whether every label is within kLocR of its pixel,
   //    which lets the passes take the packed-key kernel)
-  const bool loc = loc_begin(h);
-  static const int remap_kind = [] { const char* e = getenv("VD_REMAP"); return e ? atoi(e) : 1; }();
+  static const int remap_kind = [] { const char* e = getenv("VD_REMAP"); return e ? atoi(e) : 0; }();
+  if ((st = timed_begin(h))) return st;  // timed as an interval with k = 0 (vd_pass_times)
   for (auto& sh : h->shards) {
     if (remap_kind == 1)
       vdk::remap_lanes<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
@@ -1254,6 +1339,7 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
                                                                h->fwd, (int)sh.row0, loc ? h->loc : nullptr);
     if ((st = after_launch(h, "remap"))) return st;
   }
+  if ((st = timed_end(h, 0, 0))) return st;
   h->loc_valid = loc;
   // 3. re-stamp the new seed pixels; fwd back to all-EMPTY
   for (size_t g = 0; g < h->shards.size(); ++g) {
@@ -1276,6 +1362,7 @@ vd_status vd_set_labels(vd_handle h, const uint32_t* labels) {
   CHECK_HANDLE(h);
   if (!labels) return VD_ERR_ARG;
   DeviceGuard guard(h->device);
+  loc_forget(h);
   uint64_t rows_total = 0;
   for (auto& sh : h->shards) rows_total += sh.rows;
   const uint64_t n = rows_total * h->N;
@@ -1309,6 +1396,7 @@ vd_status vd_pass(vd_handle h, uint32_t k, uint32_t flags) {
   // A complete map (no EMPTY, known on every shard of this handle) stays complete under a
   // pass, so the EMPTY-free kernels apply; across ranks completeness is not known globally.
   const bool may_empty = !h->has_diagram || h->world > 1;
+  loc_forget(h);
   return run_pass(h, k, may_empty, (flags & VD_PASS_VON_NEUMANN) != 0);
 }
 
@@ -1552,13 +1640,16 @@ vd_status vd_pass_timing(vd_handle h, double* ms, uint64_t* launches, uint64_t* 
   DeviceGuard guard(h->device);
   if (vd_status st_ = sync_stream(h)) return st_;
   double total = 0.0;
+  uint64_t passes = 0;
   for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+    if (h->ev_k[i / 2] == 0) continue;  // a remap interval, not a pass
     float t = 0.f;
     CK(cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]));
     total += t;
+    ++passes;
   }
   if (ms) *ms = total;
-  if (launches) *launches = h->timed_launches;
+  if (launches) *launches = passes;
   if (pixels) *pixels = h->timed_px;
   h->ev_used = 0;
   h->timed_launches = 0;

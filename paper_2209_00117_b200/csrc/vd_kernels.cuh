@@ -47,6 +47,7 @@ struct PassArgs {
   int32_t res_in_y; // grid order: 0 = (x-block, segment, residue), 1 = (x-block, residue, segment)
   int32_t nwalk;    // jump_pass_sk: > 0 = whole residue classes, nwalk of them per CTA (FULL walks)
   int32_t tmap;     // jump_pass_sk, k >= 256, one band: stage each row's six spans with ONE tensor copy
+  const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label)
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
@@ -811,19 +812,27 @@ __device__ __forceinline__ uint32_t min9_sk(const RowS<4 + 2 * KS>& A, const Row
 }
 
 // One CTA of the shared-term pass (see walk() for the staging and the walk structure).
-// KM: 1 or 2 (adjacent, KS = k), 4 .. 64 (stride with k == KM known at compile time), 128 (stride,
-// any k >= 128).  FULL: the CTA runs a.nwalk whole residue classes (a one-band pass whose classes
+// KM: 1 or 2 (adjacent, KS = k), 4 .. 4096 (stride with k == KM known at compile time), 8192
+// (stride, any larger k).  FULL: the CTA runs a.nwalk whole residue classes (a one-band pass whose classes
 // have at most a.walk rows: JFA's large steps); their neighbour rows outside the grid are not
 // staged at all (the centre row is reused from registers), and the classes' rows are all staged
 // at entry, so one CTA hides the staging latency of several short walks.  Otherwise the CTA
 // runs one walk segment of a.walk rows starting at y0, as jump_pass_fast.
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL>
+//
+// REMAP (NEXT-1, the first pass of a dJFA step, one band, stride steps 4 <= k <= 128): the
+// input holds the previous frame's labels, except the new seed pixels, which hold their new
+// label with bit 31 set (stamp_flagged).  Every slot label is remapped as the thread reads it
+// from the stage -- labels[p] <- fwd[labels[p]] (Alg. 1's reuse of VD_{t-1}; R-9),
+// flagged labels unflagged -- so the remapped diagram is never written to HBM.  The gathers of
+// row j + 3 are issued while output row j is computed (one row of look-ahead), and neighbouring
+// lanes mostly ask for the same fwd entry, which the L1 serves once per warp instruction.
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false>
 __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
                                         uint32_t* smem) {
   constexpr int KS = KM < kVec ? KM : 1;
   constexpr int NS = 4 + 2 * KS;
   constexpr bool STRIDE = KM >= kVec;
-  constexpr int KC = (STRIDE && KM <= 128) ? KM : 0;  // compile-time step: immediate offsets
+  constexpr int KC = (STRIDE && KM <= 4096) ? KM : 0;  // compile-time step: immediate offsets
   const int k = KC ? KC : a.k, N = a.N;
   const int tid = (int)threadIdx.x;
   // FULL: walks y0 + w (w < nw), each of nout rows; stage slot of (walk w, row j) = w * nout + j.
@@ -831,11 +840,12 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   const int nw = FULL ? min(a.nwalk, k - (y0 - a.y_lo)) : 1;
   const int nout = FULL ? (a.y_hi - y0 + k - 1) >> a.lk : min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
   const int nlist = FULL ? nw * nout : nout + 2;
-  const bool spans = STRIDE && !KC && k >= 256;
+  const bool spans = STRIDE && k >= 256;
   const int K4 = (k + 3) & ~3;
   const int SE = stage_elems_sk(k);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
 
+  if constexpr (!PRE) {
   for (int i = tid; i < nlist; i += kThreads) mbar_init(&bars[i], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -884,6 +894,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       __syncwarp();
     }
   }
+  }  // !PRE
 
   // per-thread slot offsets in a stage, columns, and edge flags
   const uint32_t sh16 = a.sh16;
@@ -911,8 +922,26 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   uint32_t loc_acc = 0;
   bool loc_bad = false;
   using R_t = RowS<NS>;
+  // REMAP: slot labels of a staged row, remapped through fwd (loads in flight until build)
+  auto fetch = [&](int i, uint32_t (&lab)[NS]) {
+    if constexpr (!PRE) mbar_wait(&bars[i], 0u);
+    const uint32_t* st = smem + (size_t)i * SE;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) lab[s] = st[sbase + s * (spans ? 128 : k)];
+    if constexpr (FIX) {
+#pragma unroll
+      for (int s = 0; s < KS; ++s) lab[s] = left_out ? lab[s + KS] : lab[s];
+#pragma unroll
+      for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t c = lab[s];
+      lab[s] = (c & 0x80000000u) ? (c ^ 0x80000000u) : __ldg(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu)));
+    }
+  };
   auto consume = [&](int i, R_t& R) {
-    mbar_wait(&bars[i], 0u);
+    if constexpr (!PRE) mbar_wait(&bars[i], 0u);
     const uint32_t* st = smem + (size_t)i * SE;
     uint32_t lab[NS];
     if constexpr (!STRIDE) {
@@ -941,7 +970,15 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   // rows 0 and n + 1 in the stage (outside the grid: the centre row is a duplicate candidate).
   auto run = [&](int yw, int n, int ibase) {
     R_t r0, r1, r2;
-    if constexpr (FULL) {
+    uint32_t pend[NS];  // REMAP: the next row's remapped slot labels
+    if constexpr (REMAP) {
+      uint32_t l0[NS];
+      fetch(ibase, l0);
+      fetch(ibase + 1, pend);
+      build_sk<KS, MAY_EMPTY, PACK>(l0, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, r0);
+      build_sk<KS, MAY_EMPTY, PACK>(pend, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, r1);
+      fetch(ibase + 2, pend);
+    } else if constexpr (FULL) {
       consume(ibase + 1, r1);
       r0 = r1;
     } else {
@@ -952,7 +989,10 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
     uint32_t* po = a.out + (int64_t)(yw - a.row0) * a.pitch + X;
     int j = 0;
     auto step = [&](const R_t& Pv, const R_t& Cv, R_t& Nx) -> bool {
-      if (!FULL || j + 1 < n) consume(ibase + j + 2, Nx);
+      if constexpr (REMAP) {
+        build_sk<KS, MAY_EMPTY, PACK>(pend, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, Nx);
+        if (j + 3 < n + 2) fetch(ibase + j + 3, pend);  // gathers in flight during this row
+      } else if (!FULL || j + 1 < n) consume(ibase + j + 2, Nx);
       else Nx = Cv;
       uint32_t o[kVec];
       if constexpr (PACK) {
@@ -1014,10 +1054,12 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   }
 }
 
+__host__ __device__ constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2_c(v / 2); }
+
 // grid (xblocks, segs, residues) as jump_pass_fast; with a.nwalk > 0 (FULL) the z index counts
 // groups of a.nwalk residue classes.  Host: N % 512 == 0, k a power of two, k <= N / 4;
-// Euclidean Moore passes, no window (N <= 32768).  KM: k itself for k <= 128 (compile-time
-// step), 256 for any larger k.
+// Euclidean Moore passes, no window (N <= 32768).  KM: k itself for k <= 4096 (compile-time
+// step), 8192 for any larger k.
 template <int KM, bool MAY_EMPTY, bool BANDED>
 __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
@@ -1034,12 +1076,12 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
     x0 = xb * kW;
     X = x0 + kVec * tid;
     fix = x0 == 0 || x0 + kW >= a.N;
-  } else if (KM <= 128) {  // k == KM
+  } else if constexpr (KM <= 128) {  // k == KM
     x0 = xb * kW;
     X = x0 + 4 * KM * (tid / KM) + (tid % KM);
     fix = x0 == 0 || x0 + kW >= a.N;
   } else {
-    const int lr = a.lk - 7;  // k / 128 residue blocks per group of 4k columns
+    const int lr = (KM <= 4096 ? ilog2_c(KM) : a.lk) - 7;  // k / 128 residue blocks per group of 4k columns
     const int g = xb >> lr, rb = xb & ((1 << lr) - 1);
     x0 = 4 * k * g + 128 * rb;
     X = x0 + tid;
@@ -1059,6 +1101,30 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
   }
   if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, false>(a, &tm, x0, X, y0, dyn_smem);
   else walk_sk<KM, MAY_EMPTY, BANDED, false, false, false>(a, &tm, x0, X, y0, dyn_smem);
+}
+
+// The first pass of a dJFA step with the remap fused in (walk_sk REMAP): one band, stride steps
+// 4 <= k <= 128.
+template <int KM>
+__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk_remap(PassArgs a, const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(128) uint32_t dyn_smem[];
+  const int xb = (int)blockIdx.x;
+  const int seg = (int)(a.res_in_y ? blockIdx.z : blockIdx.y), res = (int)(a.res_in_y ? blockIdx.y : blockIdx.z);
+  const int y0 = a.y_lo + res + seg * a.walk * a.k;
+  if (res >= a.k || y0 >= a.y_hi) return;
+  const int tid = (int)threadIdx.x;
+  const int x0 = xb * kW;
+  const int X = x0 + 4 * KM * (tid / KM) + (tid % KM);
+  const bool fix = x0 == 0 || x0 + kW >= a.N;
+  // packed walk when the previous frame's diagram was local and the moves keep every
+  // candidate within the packed key's range (the host passes loc_in only then)
+  if (a.loc_in && *(volatile const uint32_t*)a.loc_in == 0u) {
+    if (fix) walk_sk<KM, false, false, true, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    else walk_sk<KM, false, false, false, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    return;
+  }
+  if (fix) walk_sk<KM, false, false, true, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+  else walk_sk<KM, false, false, false, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
 }
 
 // ------------------------------------------------------------------ wide jump pass
@@ -1286,6 +1352,26 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
   }
 }
 
+// Fused dJFA frame (NEXT-1): re-stamp the new seed pixels of this band BEFORE the first pass,
+// with bit 31 set so that the pass's in-stage remap leaves them as they are (R-9: remap, then
+// re-stamp).  Labels are < 2^31 (N <= 32768), so the flag is free.
+__global__ void stamp_flagged(uint32_t* __restrict__ g, int64_t pitch, int row0, int rows,
+                              const uint32_t* __restrict__ new_s, int64_t s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = new_s[i];
+    const int y = (int)(c >> 16) - row0, x = (int)(c & 0xFFFFu);
+    if (y >= 0 && y < rows) g[(int64_t)y * pitch + x] = c | 0x80000000u;
+  }
+}
+
+// ... and after it: fwd back to all-EMPTY (its entries at the old seed pixels).
+__global__ void fwd_reset(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s, int64_t s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = old_s[i];
+    fwd[(int64_t)(o >> 16) * N + (o & 0xFFFFu)] = EMPTY;
+  }
+}
+
 // Reuse VD_{t-1}: every label moves with its seed, labels[p] <- fwd[labels[p]].
 // Neighbouring pixels mostly share a label, so the gathers hit L1.
 // Row-major sweeps below: CTAs stride over rows, threads over 4-label quads of a row, with
@@ -1327,38 +1413,57 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
   if (loc && __syncthreads_or(far) && threadIdx.x == 0) atomicOr(loc, 1u);
 }
 
-// The same remap with lanes on consecutive pixels: a warp covers 32 consecutive pixels per
-// access (four such groups per thread and round), so one gather instruction of the warp
-// touches the fwd entries of the 2-3 seeds whose regions cross those 32 pixels instead of
-// the 8-10 seeds of a 128-pixel span (fewer L1 wavefronts per gather).  Same result and the
-// same locality flag as remap().
+// The same remap with lanes on consecutive pixels, software-pipelined.  A warp covers 128
+// consecutive pixels of a row per round (lane t: pixels x0 + t + 32 e, e < 4), so one gather
+// instruction touches the fwd entries of the 2-3 seeds whose regions cross 32 pixels.  The
+// remap is latency-bound (a DRAM load of the labels, then a dependent L2 gather of fwd), so
+// each thread loads the labels of its NEXT round before it gathers and stores the current one:
+// the two latencies overlap instead of adding up.  Same result and locality flag as remap().
 __global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd,
                             int row0, uint32_t* __restrict__ loc) {
   uint32_t mx = 0;
   const int lane = (int)threadIdx.x & 31, warp = (int)threadIdx.x >> 5, nwarps = (int)blockDim.x >> 5;
-  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+  // the warp's rounds: (row r, chunk x0) in row-major order over this CTA's rows
+  const uint32_t per_row = (uint32_t)(N + 127) / 128u;
+  const int nround = ((rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * (int)per_row;
+  auto round_at = [&](int i, int& r, int& x0) {
+    const uint32_t q = (uint32_t)i / per_row;
+    r = (int)blockIdx.x + (int)q * (int)gridDim.x;
+    x0 = (int)((uint32_t)i - q * per_row) * 128;
+  };
+  auto load = [&](int i, uint32_t (&c)[4]) {
+    int r, x0;
+    round_at(i, r, x0);
+    const uint32_t* row = g + (int64_t)r * pitch;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int x = x0 + 32 * e + lane;
+      c[e] = x < N ? row[x] : EMPTY;
+    }
+  };
+  uint32_t cur[4], nxt[4] = {EMPTY, EMPTY, EMPTY, EMPTY};
+  int i = warp;
+  if (i < nround) load(i, cur);
+  for (; i < nround; i += nwarps) {
+    if (i + nwarps < nround) load(i + nwarps, nxt);  // next round's labels: in flight during the gathers
+    uint32_t nc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      nc[e] = cur[e] != EMPTY ? __ldg(fwd + (int64_t)(cur[e] >> 16) * N + (cur[e] & 0xFFFFu)) : EMPTY;
+    int r, x0;
+    round_at(i, r, x0);
     uint32_t* row = g + (int64_t)r * pitch;
     const uint32_t nb = __vsub2(0x002C002Cu, ((uint32_t)(row0 + r) << 16));  // (44 - y, 44) per lane
-#pragma unroll 2
-    for (int x0 = 128 * warp; x0 < N; x0 += 128 * nwarps) {
-      uint32_t c[4], nc[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int x = x0 + 32 * e + lane;
-        c[e] = x < N ? row[x] : EMPTY;
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        nc[e] = c[e] != EMPTY ? __ldg(fwd + (int64_t)(c[e] >> 16) * N + (c[e] & 0xFFFFu)) : EMPTY;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int x = x0 + 32 * e + lane;
-        if (x < N) {
-          row[x] = nc[e];
-          mx = __vmaxu2(mx, nc[e] == EMPTY ? 0xFFFFFFFFu : __vadd2(nc[e], __vsub2(nb, (uint32_t)x)));
-        }
+    for (int e = 0; e < 4; ++e) {
+      const int x = x0 + 32 * e + lane;
+      if (x < N) {
+        row[x] = nc[e];
+        mx = __vmaxu2(mx, nc[e] == EMPTY ? 0xFFFFFFFFu : __vadd2(nc[e], __vsub2(nb, (uint32_t)x)));
       }
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
   }
   const bool far = (mx >> 16) > 88u || (mx & 0xFFFFu) > 88u;
   if (loc && __syncthreads_or(far) && threadIdx.x == 0) atomicOr(loc, 1u);

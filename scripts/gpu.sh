@@ -12,6 +12,7 @@
 #   ncupass   ncu --set full of one dJFA frame's jump passes (C4) + source page
 #   ncujfa    ncu --set full of one JFA frame's jump passes (C4)
 #   ncuremap  ncu --set full of the remap kernel (C4)
+#   c4launch  ncu launch list (durations + DRAM bytes) of C4 JFA + 3 dJFA frames
 #   c5launch  ncu launch list (durations + DRAM bytes) of C5 JFA + dJFA frames
 #   variants  scripts/time_variants.py (build/variants/*.so)
 #   skab      A/B of the shared-term pass kernel (VD_NO_SK=1 vs 0), per-k pass times
@@ -40,6 +41,7 @@ ncujfa) VD_FRAMES=0 timeout 900 ncu --set full --clock-control none --import-sou
 ncuremap) timeout 900 ncu --set full --clock-control none --import-source on -k regex:remap -c 1 -o /tmp/prof_remap_$TAG python scripts/profile_pass.py > /dev/null 2>&1
   ncu -i /tmp/prof_remap_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_remap_${TAG}_raw.csv 2>/dev/null
   ncu -i /tmp/prof_remap_$TAG.ncu-rep --page source --csv --print-source sass -k regex:remap -c 1 > gpurun_out/prof_remap_${TAG}_src.csv 2>/dev/null ;;
+c4launch) timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c4_launches_$TAG.csv python scripts/profile_pass.py > gpurun_out/c4_launches_$TAG.log 2>&1 ;;
 c5launch) VD_CFG=C5 VD_FRAMES=2 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c5_launches_$TAG.csv python scripts/profile_pass.py > gpurun_out/c5_launches_$TAG.log 2>&1 ;;
 variants) timeout 1500 python scripts/time_variants.py 2>&1 | tee gpurun_out/variants_$TAG.txt ;;
 skab) timeout 900 python scripts/time_variants.py VD_NO_SK=1,0 2>&1 | tee gpurun_out/skab_$TAG.txt ;;
