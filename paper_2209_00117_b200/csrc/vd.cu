@@ -538,6 +538,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.nwalk = 0;
   a.tmap = 0;
   a.fwd = nullptr;
+  a.prefetch = 0;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
   a.top = sh.top[h->hpar];
@@ -640,6 +641,8 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
       if (k >= 256 && !banded && !no_tmap && encode_span_map(h, a.in, sh.rows, k, &tm)) a.tmap = 1;
       if (h->fuse_remap) {  // first dJFA pass with the remap fused in (vd_djfa_step checked the conditions)
         a.fwd = h->fwd;
+        static const int pf = [] { const char* e = getenv("VD_FUSE_PF"); return e ? atoi(e) : 0; }();
+        a.prefetch = pf;
         a.loc_in = h->pass_loc_in;  // the previous frame's locality, when the moves keep the packed key valid
         a.nwalk = 0;
         const dim3 g2((unsigned)a.xblocks, a.res_in_y ? nres : (unsigned)a.segs, a.res_in_y ? (unsigned)a.segs : nres);

@@ -48,6 +48,7 @@ struct PassArgs {
   int32_t nwalk;    // jump_pass_sk: > 0 = whole residue classes, nwalk of them per CTA (FULL walks)
   int32_t tmap;     // jump_pass_sk, k >= 256, one band: stage each row's six spans with ONE tensor copy
   const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label)
+  int32_t prefetch;     // jump_pass_sk_remap: also pull the fwd lines of the row after next into L1
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
@@ -992,6 +993,16 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       if constexpr (REMAP) {
         build_sk<KS, MAY_EMPTY, PACK>(pend, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, Nx);
         if (j + 3 < n + 2) fetch(ibase + j + 3, pend);  // gathers in flight during this row
+        if (a.prefetch && j + 4 < n + 2) {  // and the row after that: its fwd lines into L1
+          mbar_wait(&bars[ibase + j + 4], 0u);
+          const uint32_t* st = smem + (size_t)(ibase + j + 4) * SE;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const uint32_t c = st[sbase + s * (spans ? 128 : k)];
+            if (!(c & 0x80000000u))
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu))));
+          }
+        }
       } else if (!FULL || j + 1 < n) consume(ibase + j + 2, Nx);
       else Nx = Cv;
       uint32_t o[kVec];
