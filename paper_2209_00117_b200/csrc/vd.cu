@@ -607,7 +607,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     unsigned gz = a.res_in_y ? (unsigned)a.segs : nres, gy = a.res_in_y ? nres : (unsigned)a.segs;
     if (sk && !h->fuse_remap && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
       const uint32_t per = h->N / k, fit = (uint32_t)vdk::walk_len_sk((int)k) + 2;
-      if (2 * per <= fit) {  // (one class per CTA measured no faster than segment walks)
+      if (4 * per <= fit) {  // (one or two classes per CTA measured slower than segment walks)
         // as many classes per CTA as fit, but keep >= 4 CTAs per SM in the grid
         const int64_t cap = std::max<int64_t>(1, (int64_t)a.xblocks * k / ((int64_t)h->num_sms * 4));
         a.nwalk = (int)std::min<int64_t>(fit / per, cap);
@@ -641,7 +641,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
       if (k >= 256 && !banded && !no_tmap && encode_span_map(h, a.in, sh.rows, k, &tm)) a.tmap = 1;
       if (h->fuse_remap) {  // first dJFA pass with the remap fused in (vd_djfa_step checked the conditions)
         a.fwd = h->fwd;
-        static const int pf = [] { const char* e = getenv("VD_FUSE_PF"); return e ? atoi(e) : 0; }();
+        static const int pf = [] { const char* e = getenv("VD_FUSE_PF"); return e ? atoi(e) : 1; }();
         a.prefetch = pf;
         a.loc_in = h->pass_loc_in;  // the previous frame's locality, when the moves keep the packed key valid
         a.nwalk = 0;
