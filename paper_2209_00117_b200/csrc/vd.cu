@@ -181,6 +181,7 @@ struct vd_ctx {
   bool pass_loc_used = false;             // some launch of the pass could take the packed walk
   bool fuse_remap = false;                // the next pass remaps its staged rows (NEXT-1, jump_pass_sk_remap)
   bool fuse_pack = false;                 // ... and may take the packed walk (previous flag + move bound)
+  bool in_djfa = false;                   // passes of a vd_djfa_step are running
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -448,12 +449,18 @@ cudaError_t launch_fast_k(int dev, bool me, bool bd, bool rel, int metric, bool 
 // k in {1, 2} (adjacent columns) or 32 <= k <= N/4 (stride columns).  VD_NO_SK=1 disables it
 // (A/B timing).
 // VD_SK_MASK (hex bitmask over log2 k) selects the steps it takes, for A/B timing.
-bool sk_ok(const vd_ctx* h, uint32_t k, bool vn, bool rel) {
+// Beyond N = 32768 it takes complete diagrams with k <= 64 (dJFA's passes): packed walk when the
+// input is local, else exact 64-bit keys; the rest stays on the windowed / wide kernels.
+bool sk_ok(const vd_ctx* h, uint32_t k, bool vn, bool may_empty) {
   static const bool off = [] { const char* e = getenv("VD_NO_SK"); return e && e[0] == '1'; }();
   static const uint64_t mask = [] { const char* e = getenv("VD_SK_MASK"); return e ? strtoull(e, nullptr, 16) : ~0ull; }();
   uint32_t lk = 0;
   while ((1u << lk) < k) ++lk;
-  return !off && ((mask >> lk) & 1) && !rel && !vn && h->metric == 0 && h->N % 512 == 0 && 4 * k <= h->N;
+  // beyond 32768 only inside dJFA frames, whose inputs are local (packed walk); JFA's passes there
+  // are never local and keep the windowed exact walk, which beats 64-bit keys
+  if (h->force_rel || (h->N > 32768 && (may_empty || k > (uint32_t)vdk::kPackMaxK || !h->in_djfa))) return false;
+  if (may_empty && h->N > 16384) return false;  // the virtual far seed needs 2N - 1 < 2^15 (as jump_pass_fast)
+  return !off && ((mask >> lk) & 1) && !vn && h->metric == 0 && h->N % 512 == 0 && 4 * k <= h->N;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (libvd does not link libcuda).
@@ -574,11 +581,11 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.y_hi = (int)y_hi;
   const uint32_t R = (uint32_t)(y_hi - y_lo);  // output rows of this launch
   if (R == 0) return VD_OK;
-  const bool rel = rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096);
-  if ((fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
+  const bool sk = sk_ok(h, k, vn, may_empty) && (k & (k - 1)) == 0;
+  const bool rel = !sk && (rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096));
+  if ((sk || fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, R);
     const uint32_t per_res = (R + k - 1) / k;
-    const bool sk = sk_ok(h, k, vn, rel);
     a.walk = sk ? vdk::walk_len_sk((int)k) : vdk::walk_len((int)k, rel);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     // Small grids (C2: 1024^2 at k = 1 is 2 x 1 x 43 walks of 24 rows): shorten the walks until
@@ -1287,6 +1294,11 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   }
   std::vector<uint32_t> ks;
   schedule_djfa(h->N, h->s, d_max, h->extras, ks);
+  struct InDjfa {
+    vd_ctx* h;
+    ~InDjfa() { h->in_djfa = false; }
+  } in_djfa{h};
+  h->in_djfa = true;
   const short2* dd;
   int slot;
   vd_status st = upload_disp(h, disp_xy, &dd, &slot);
@@ -1303,7 +1315,7 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   static const bool no_fuse = [] { const char* e = getenv("VD_NO_FUSE"); return e && e[0] == '1'; }();
   const uint32_t k1 = ks[0];
   const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->N <= 32768 &&
-                    !h->force_rel && sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
+                    sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
   if (fuse) {
     Shard& sh = h->shards[0];
     vdk::stamp_flagged<<<gs, 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0, (int)sh.rows, h->seeds_new,

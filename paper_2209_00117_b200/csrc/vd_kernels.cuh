@@ -827,7 +827,26 @@ __device__ __forceinline__ uint32_t min9_sk(const RowS<4 + 2 * KS>& A, const Row
 // flagged labels unflagged -- so the remapped diagram is never written to HBM.  The gathers of
 // row j + 3 are issued while output row j is computed (one row of look-ahead), and neighbouring
 // lanes mostly ask for the same fwd entry, which the L1 serves once per warp instruction.
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false>
+// X64 (grids beyond N = 32768, whose labels are not all local): the same walk with the exact key
+// evaluated in 64 bits per candidate (consider64); the packed walk needs no such fallback, since
+// its arithmetic is mod 2^32 (jump_pass_fast's windowed kernel relies on the same property).
+template <int KS>
+__device__ __forceinline__ uint32_t best64_sk(const RowS<4 + 2 * KS>& A, const RowS<4 + 2 * KS>& B,
+                                              const RowS<4 + 2 * KS>& Cn, int e, int xe, int y) {
+  uint64_t bd = ~0ull;
+  uint32_t bc = EMPTY;
+  const RowS<4 + 2 * KS>* rows[3] = {&A, &B, &Cn};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    consider64<0>(rows[j]->c[e], xe, y, bd, bc);
+    consider64<0>(rows[j]->c[e + KS], xe, y, bd, bc);
+    consider64<0>(rows[j]->c[e + 2 * KS], xe, y, bd, bc);
+  }
+  return bc;
+}
+
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false,
+          bool X64 = false>
 __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
                                         uint32_t* smem) {
   constexpr int KS = KM < kVec ? KM : 1;
@@ -1006,7 +1025,11 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       } else if (!FULL || j + 1 < n) consume(ibase + j + 2, Nx);
       else Nx = Cv;
       uint32_t o[kVec];
-      if constexpr (PACK) {
+      if constexpr (X64) {
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) o[e] = best64_sk<KS>(Pv, Cv, Nx, e, STRIDE ? X + e * k : X + e, y);
+        loc_bad = true;  // not tracked on this path
+      } else if constexpr (PACK) {
         const uint32_t uy = (uint32_t)y;
         const uint32_t My = 256u - (uy << 17);
         const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
@@ -1108,6 +1131,13 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
       if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, true, false>(a, &tm, x0, X, y0, dyn_smem);
       else walk_sk<KM, MAY_EMPTY, BANDED, false, true, false>(a, &tm, x0, X, y0, dyn_smem);
       return;
+    }
+    if constexpr (KM <= 64) {
+      if (a.N > 32768) {  // 32-bit squared distances would overflow: exact 64-bit keys
+        if (fix) walk_sk<KM, false, BANDED, true, false, false, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, false, false, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+        return;
+      }
     }
   }
   if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, false>(a, &tm, x0, X, y0, dyn_smem);

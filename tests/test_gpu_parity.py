@@ -464,6 +464,24 @@ def test_windowed_pass_with_empty_bit_exact(vd, rel_grid, k):
 
 
 @pytest.mark.slow
+def test_djfa_beyond_32768_sparse_seeds_bit_exact(vd):
+    # A dJFA frame on a grid beyond 32768 (33280 = 65 * 512) with sparse seeds: the labels are far
+    # from their pixels, so the shared-term kernel's small steps take its exact 64-bit walk (X64),
+    # and the large steps the windowed / 64-bit kernels.  Every pixel against the oracle.
+    N, s, dmax = 33280, 2000, 3
+    xy = synth.uniform_seeds(N, s, rng_seed=33)
+    d = _jfa_gpu(vd, N, xy)
+    G = oracle.jfa(N, xy)
+    assert np.array_equal(d.labels(), G)
+    disp = synth.displacements(s, dmax, 0, rng_seed=33)
+    d.djfa_step(disp, dmax)
+    G, xy, n = oracle.djfa_step(N, xy, disp, dmax, G, inplace=True)
+    assert d.last_passes() == n and d.last_packed_passes() == 0
+    assert np.array_equal(d.labels(), G)
+    d.close()
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("N,s", [(20000, 25000), (33000, 4000)])
 def test_jfa_large_grid_bit_exact(vd, N, s):
     # JFA beyond the plain fast kernel's range: the 64-bit kernel while EMPTY remains, then
