@@ -388,8 +388,8 @@ def run_gpu(args):
     hashes = torch.zeros(len(disp_pin), dtype=torch.int64).pin_memory()  # each step's result
     x0.record(stream)
     for i, a in enumerate(disp_pin):
-        vd.vd_djfa_step(dj.h, a, d, s)
-        vd.vd_label_hash_async(dj.h, hashes[i].data_ptr())  # D2H without a host round trip
+        # the step's last pass also sums the checksum; 8-byte D2H without a host round trip
+        vd.vd_djfa_step_hash(dj.h, a, d, s, hashes[i].data_ptr())
     x1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(x0.elapsed_time(x1))
@@ -494,9 +494,9 @@ def run_gpu(args):
             "parity": parity,
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 4 * s, "d2h_bytes_per_step": 8,
                     "steps": len(disp_pin),
-                    "what": ("vd_djfa_step with pinned host displacements + vd_label_hash_async per step; the step's "
-                             "result read back is an 8-byte checksum of the whole label map (a consumer of the map "
-                             "itself: see e2e_full_map)")},
+                    "what": ("vd_djfa_step_hash with pinned host displacements per step: the dJFA step, whose last "
+                             "pass also sums the new diagram's checksum; the result read back is that 8-byte checksum "
+                             "of the whole label map (a consumer of the map itself: see e2e_full_map)")},
             "e2e_full_map": e2e_full,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -136,6 +136,13 @@ vd_status vd_move_seeds(vd_handle h, const int16_t* disp_xy);
  * complete, but the library does not check the displacements against it. */
 vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max);
 
+/* vd_djfa_step followed by vd_label_hash_async, with the checksum accumulated by the step's last
+ * jump pass where it can (Euclidean Moore step 1 on grids with N % 512 == 0; else a separate
+ * label_hash kernel): *pinned_out (pinned host memory) receives the new diagram's vd_label_hash
+ * when the handle's stream reaches that point; the call itself only enqueues.  Summed over
+ * ranks when world > 1.  Errors as vd_djfa_step; VD_ERR_ARG if pinned_out is NULL. */
+vd_status vd_djfa_step_hash(vd_handle h, const int16_t* disp_xy, uint32_t d_max, uint64_t* pinned_out);
+
 /* Replace the current diagram with a host label map (N*N dense; this rank's band when
  * world > 1).  Every label must be EMPTY or an in-grid position (else VD_ERR_RANGE; the
  * reserved pixel is EMPTY itself at N = 65536).  Afterwards the handle holds "a diagram"

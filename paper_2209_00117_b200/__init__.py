@@ -21,7 +21,7 @@ import numpy as np
 __all__ = [
     "VDError", "load_library", "library_path", "VoronoiDiagram", "EMPTY",
     "vd_config", "vd_halo_plan_t", "vd_create", "vd_destroy", "vd_jfa", "vd_move_seeds",
-    "vd_djfa_step", "vd_stf", "vd_get_labels_into", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
+    "vd_djfa_step", "vd_djfa_step_hash", "vd_stf", "vd_get_labels_into", "vd_similarity", "vd_similarity_host", "vd_label_hash", "vd_get_labels",
     "vd_get_seeds", "vd_band", "vd_last_passes", "vd_last_packed_passes", "vd_synchronize", "vd_set_pass_timing",
     "vd_pass_timing", "vd_pass_times", "vd_launch_count", "vd_schedule_jfa", "vd_schedule_djfa",
     "vd_halo_plan", "vd_nccl_unique_id", "vd_status_str", "vd_set_labels", "vd_pass", "vd_peer_export",
@@ -85,6 +85,7 @@ _SIGS = {
     "vd_stf": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint32)]),
     "vd_move_seeds": (ctypes.c_int32, [H, P]),
     "vd_djfa_step": (ctypes.c_int32, [H, P, ctypes.c_uint32]),
+    "vd_djfa_step_hash": (ctypes.c_int32, [H, P, ctypes.c_uint32, P]),
     "vd_similarity": (ctypes.c_int32, [H, H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "vd_similarity_host": (ctypes.c_int32, [H, P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "vd_label_hash": (ctypes.c_int32, [H, ctypes.POINTER(ctypes.c_uint64)]),
@@ -239,6 +240,14 @@ def vd_move_seeds(h, disp_xy, s: int) -> None:
 def vd_djfa_step(h, disp_xy, d_max: int, s: int) -> None:
     ptr, keep = _addr(disp_xy, np.int16, 2 * s)
     _check(load_library().vd_djfa_step(h, ptr, d_max), "vd_djfa_step", h)
+    del keep
+
+
+def vd_djfa_step_hash(h, disp_xy, d_max: int, s: int, pinned_out: int) -> None:
+    """vd_djfa_step + the new diagram's label checksum into pinned host memory at pinned_out
+    (e.g. a pinned torch.int64 tensor's data_ptr()); enqueue only."""
+    ptr, keep = _addr(disp_xy, np.int16, 2 * s)
+    _check(load_library().vd_djfa_step_hash(h, ptr, d_max, ctypes.c_void_p(pinned_out)), "vd_djfa_step_hash", h)
     del keep
 
 

@@ -182,6 +182,7 @@ struct vd_ctx {
   bool fuse_remap = false;                // the next pass remaps its staged rows (NEXT-1, jump_pass_sk_remap)
   bool fuse_pack = false;                 // ... and may take the packed walk (previous flag + move bound)
   bool in_djfa = false;                   // passes of a vd_djfa_step are running
+  bool hash_pass = false;                 // the running pass also accumulates the label checksum
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -489,18 +490,18 @@ bool encode_span_map(const vd_ctx* h, const uint32_t* in, uint32_t rows, uint32_
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int KM, bool ME, bool BD>
+template <int KM, bool ME, bool BD, bool HASH = false>
 cudaError_t launch_sk(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk, size_t sm,
                       cudaStream_t st) {
   static std::atomic<uint64_t> opted{0};
   const uint64_t bit = 1ull << (dev & 63);
   if (!(opted.load(std::memory_order_acquire) & bit)) {
-    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk<KM, ME, BD>,
+    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk<KM, ME, BD, HASH>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, vdk::kSmemBudget);
     if (e != cudaSuccess) return e;
     opted.fetch_or(bit, std::memory_order_release);
   }
-  vdk::jump_pass_sk<KM, ME, BD><<<grid, blk, sm, st>>>(a, tm);
+  vdk::jump_pass_sk<KM, ME, BD, HASH><<<grid, blk, sm, st>>>(a, tm);
   return cudaSuccess;
 }
 template <int KM>
@@ -546,6 +547,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.tmap = 0;
   a.fwd = nullptr;
   a.prefetch = 0;
+  a.hash_out = nullptr;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
   a.top = sh.top[h->hpar];
@@ -663,7 +665,15 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
         }
       } else
       switch (k) {
-        case 1: e = launch_sk_k<1>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 1:
+          if (h->hash_pass && !may_empty) {  // the frame's last pass also sums the label checksum
+            a.hash_out = h->counter;
+            e = banded ? launch_sk<1, false, true, true>(h->device, a, tm, grid, blk, sm, h->stream)
+                       : launch_sk<1, false, false, true>(h->device, a, tm, grid, blk, sm, h->stream);
+          } else {
+            e = launch_sk_k<1>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+          }
+          break;
         case 2: e = launch_sk_k<2>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 4: e = launch_sk_k<4>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 8: e = launch_sk_k<8>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
@@ -1282,11 +1292,11 @@ vd_status vd_move_seeds(vd_handle h, const int16_t* disp_xy) {
   return VD_OK;
 }
 
-vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
-  CHECK_HANDLE(h);
-  if (!disp_xy) return VD_ERR_ARG;
-  if (!h->has_diagram) return fail(h, VD_ERR_STATE, "vd_djfa_step needs a diagram: call vd_jfa first");
-  DeviceGuard guard(h->device);
+namespace {
+vd_status enqueue_label_hash(vd_ctx* h);
+// One dJFA step (vd_djfa_step).  hash: also leave the new diagram's label checksum in h->counter,
+// accumulated by the last pass when it can (jump_pass_sk HASH, k = 1), else by label_hash.
+vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash) {
   NvtxRange range("vd_djfa_step");
   if (!h->fwd) {  // forward map, kept all-EMPTY between steps
     CK(cudaMalloc(&h->fwd, (size_t)h->N * h->N * sizeof(uint32_t)));
@@ -1296,9 +1306,12 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   schedule_djfa(h->N, h->s, d_max, h->extras, ks);
   struct InDjfa {
     vd_ctx* h;
-    ~InDjfa() { h->in_djfa = false; }
+    ~InDjfa() { h->in_djfa = h->hash_pass = false; }
   } in_djfa{h};
   h->in_djfa = true;
+  // the fused checksum needs the last pass to be a Moore step 1 on jump_pass_sk
+  const bool hash_fused = hash && ks.back() == 1 && ks.size() > h->vn_waves && sk_ok(h, 1, false, false);
+  if (hash) CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
   const short2* dd;
   int slot;
   vd_status st = upload_disp(h, disp_xy, &dd, &slot);
@@ -1334,10 +1347,13 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
     vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, (int64_t)h->s);
     if ((st = after_launch(h, "fwd_reset"))) return st;
     std::swap(h->seeds, h->seeds_new);
-    for (size_t i = 1; i < ks.size(); ++i)
+    for (size_t i = 1; i < ks.size(); ++i) {
+      h->hash_pass = hash_fused && i + 1 == ks.size();
       if ((st = run_pass(h, ks[i], false, false, i + 1 < ks.size() ? ks[i + 1] : 0))) return loc_end(h), st;
+    }
     loc_end(h);
     h->last_passes = (uint32_t)ks.size();
+    if (hash && !(hash_fused && ks.size() > 1)) return enqueue_label_hash(h);
     return VD_OK;
   }
   // 2. labels follow their seeds (reuse of VD_{t-1})
@@ -1366,10 +1382,37 @@ vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
   std::swap(h->seeds, h->seeds_new);
   // 4. passes delta_1 .. 1 (Eq. 4).  The remapped diagram is complete (every label is a
   //    seed), so no EMPTY exists.
-  for (size_t i = 0; i < ks.size(); ++i)
+  for (size_t i = 0; i < ks.size(); ++i) {
+    h->hash_pass = hash_fused && i + 1 == ks.size();
     if ((st = run_pass(h, ks[i], false, i < h->vn_waves, i + 1 < ks.size() ? ks[i + 1] : 0))) return loc_end(h), st;
+  }
   loc_end(h);
   h->last_passes = (uint32_t)ks.size();
+  if (hash && !hash_fused) return enqueue_label_hash(h);
+  return VD_OK;
+}
+}  // namespace
+
+vd_status vd_djfa_step(vd_handle h, const int16_t* disp_xy, uint32_t d_max) {
+  CHECK_HANDLE(h);
+  if (!disp_xy) return VD_ERR_ARG;
+  if (!h->has_diagram) return fail(h, VD_ERR_STATE, "vd_djfa_step needs a diagram: call vd_jfa first");
+  DeviceGuard guard(h->device);
+  return djfa_step(h, disp_xy, d_max, false);
+}
+
+vd_status vd_djfa_step_hash(vd_handle h, const int16_t* disp_xy, uint32_t d_max, uint64_t* pinned_out) {
+  CHECK_HANDLE(h);
+  if (!disp_xy || !pinned_out) return VD_ERR_ARG;
+  if (!h->has_diagram) return fail(h, VD_ERR_STATE, "vd_djfa_step needs a diagram: call vd_jfa first");
+  DeviceGuard guard(h->device);
+  vd_status st = djfa_step(h, disp_xy, d_max, true);
+  if (st) return st;
+  if (h->world > 1) {
+    if (!h->comm) return fail(h, VD_ERR_STATE, "no NCCL communicator for the cross-rank sum");
+    CKN(g_nccl.AllReduce(h->counter, h->counter, 1, ncclUint64, ncclSum, h->comm, h->stream));
+  }
+  CK(cudaMemcpyAsync(pinned_out, h->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
   return VD_OK;
 }
 

@@ -49,6 +49,7 @@ struct PassArgs {
   int32_t tmap;     // jump_pass_sk, k >= 256, one band: stage each row's six spans with ONE tensor copy
   const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label)
   int32_t prefetch;     // jump_pass_sk_remap: also pull the fwd lines of the row after next into L1
+  unsigned long long* hash_out;  // jump_pass_sk<1> HASH: add the outputs' label checksum here
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
@@ -678,6 +679,32 @@ __global__ void __launch_bounds__(kThreads, REL ? VD_REL_MIN_BLOCKS : VD_MIN_BLO
   else walk<KM, MAY_EMPTY, BANDED, false, METRIC, VN, REL, false>(a, x0, y0, dyn_smem);
 }
 
+// MurmurHash3's 32-bit finaliser: the per-pixel term of the label checksum (label_hash).
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
+  __shared__ uint64_t part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) part[wid] = v;
+  __syncthreads();
+  uint64_t t = 0;
+  if (wid == 0) {
+    t = (lane < (int)(blockDim.x >> 5)) ? part[lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
 // ------------------------------------------------------------------ shared-term jump pass (r02)
 //
 // The pass of jump_pass_fast (Euclidean, Moore, N % 512 == 0), with the per-row terms of each
@@ -845,8 +872,11 @@ __device__ __forceinline__ uint32_t best64_sk(const RowS<4 + 2 * KS>& A, const R
   return bc;
 }
 
+// HASH (the last pass of an e2e dJFA step, KM = 1): every output label is also added to the
+// frame's checksum, sum over p of fmix32((y N + x) * 0x9E3779B9 ^ label) mod 2^64 (label_hash),
+// so the step needs no separate 4-B/px read for its result.
 template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false,
-          bool X64 = false>
+          bool X64 = false, bool HASH = false>
 __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
                                         uint32_t* smem) {
   constexpr int KS = KM < kVec ? KM : 1;
@@ -941,6 +971,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
 
   uint32_t loc_acc = 0;
   bool loc_bad = false;
+  uint64_t hacc = 0;  // HASH
   using R_t = RowS<NS>;
   // REMAP: slot labels of a staged row, remapped through fwd (loads in flight until build)
   auto fetch = [&](int i, uint32_t (&lab)[NS]) {
@@ -1057,6 +1088,11 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         }
         loc_bad |= mm > (int)kLocD2 - y * y;
       }
+      if constexpr (HASH) {
+        const uint32_t b = ((uint32_t)y * (uint32_t)N + (uint32_t)X) * 0x9E3779B9u;
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) hacc += fmix32((b + (uint32_t)e * 0x9E3779B9u) ^ o[e]);
+      }
       if constexpr (!STRIDE) {
         store_out(a, BANDED, y, X, po, make_uint4(o[0], o[1], o[2], o[3]));
       } else {
@@ -1086,6 +1122,10 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
     else far = loc_bad;
     if (__syncthreads_or(far) && tid == 0) atomicOr(a.loc_out, 1u);
   }
+  if constexpr (HASH) {
+    const uint64_t t = block_sum_u64(hacc);
+    if (tid == 0) atomicAdd(a.hash_out, (unsigned long long)t);
+  }
 }
 
 __host__ __device__ constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2_c(v / 2); }
@@ -1094,7 +1134,7 @@ __host__ __device__ constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2
 // groups of a.nwalk residue classes.  Host: N % 512 == 0, k a power of two, k <= N / 4;
 // Euclidean Moore passes, no window (N <= 32768).  KM: k itself for k <= 4096 (compile-time
 // step), 8192 for any larger k.
-template <int KM, bool MAY_EMPTY, bool BANDED>
+template <int KM, bool MAY_EMPTY, bool BANDED, bool HASH = false>
 __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)blockIdx.x;
@@ -1122,26 +1162,26 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
     fix = g == 0 || x0 - 128 * rb + 4 * k >= a.N;
   }
   if (full) {  // JFA's large steps: exact walk (their diagrams are never local)
-    if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
-    else walk_sk<KM, MAY_EMPTY, BANDED, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, true, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
+    else walk_sk<KM, MAY_EMPTY, BANDED, false, false, true, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
     return;
   }
   if constexpr (!MAY_EMPTY) {
     if (a.loc_in && k <= kPackMaxK && *(volatile const uint32_t*)a.loc_in == 0u) {
-      if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, true, false>(a, &tm, x0, X, y0, dyn_smem);
-      else walk_sk<KM, MAY_EMPTY, BANDED, false, true, false>(a, &tm, x0, X, y0, dyn_smem);
+      if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, true, false, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
+      else walk_sk<KM, MAY_EMPTY, BANDED, false, true, false, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
       return;
     }
     if constexpr (KM <= 64) {
       if (a.N > 32768) {  // 32-bit squared distances would overflow: exact 64-bit keys
-        if (fix) walk_sk<KM, false, BANDED, true, false, false, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
-        else walk_sk<KM, false, BANDED, false, false, false, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+        if (fix) walk_sk<KM, false, BANDED, true, false, false, false, false, true, HASH>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, false, false, false, false, true, HASH>(a, &tm, x0, X, y0, dyn_smem);
         return;
       }
     }
   }
-  if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, false>(a, &tm, x0, X, y0, dyn_smem);
-  else walk_sk<KM, MAY_EMPTY, BANDED, false, false, false>(a, &tm, x0, X, y0, dyn_smem);
+  if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, false, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
+  else walk_sk<KM, MAY_EMPTY, BANDED, false, false, false, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
 }
 
 // The first pass of a dJFA step with the remap fused in (walk_sk REMAP): one band, stride steps
@@ -1510,22 +1550,7 @@ __global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, i
   if (loc && __syncthreads_or(far) && threadIdx.x == 0) atomicOr(loc, 1u);
 }
 
-// ------------------------------------------------------------------ reductions
-__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
-  __shared__ uint64_t part[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) part[wid] = v;
-  __syncthreads();
-  uint64_t t = 0;
-  if (wid == 0) {
-    t = (lane < (int)(blockDim.x >> 5)) ? part[lane] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, o);
-  }
-  return t;  // valid in thread 0
-}
+// ------------------------------------------------------------------ reductions (block_sum_u64 above)
 
 // Eq. 5 numerator: count of pixels with equal labels in a band.
 __global__ void match_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t pitch,
@@ -1561,15 +1586,6 @@ __global__ void count_value(const uint32_t* __restrict__ g, int64_t pitch, int r
   }
   uint64_t t = block_sum_u64(cnt);
   if (threadIdx.x == 0 && t) atomicAdd(out, (unsigned long long)t);
-}
-
-__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
-  h ^= h >> 16;
-  h *= 0x85EBCA6Bu;
-  h ^= h >> 13;
-  h *= 0xC2B2AE35u;
-  h ^= h >> 16;
-  return h;
 }
 
 // Checksum sum_p fmix32((uint32)(p * 0x9E3779B9) ^ label[p]) in uint64 over a band

@@ -636,6 +636,25 @@ def test_label_hash_async_matches(vd):
     assert [int(v) & 0xFFFFFFFFFFFFFFFF for v in out] == want
 
 
+@pytest.mark.parametrize("N,s,G", [(1024, 4096, 0), (1024, 4096, 4), (1000, 3906, 0), (512, 100, 0)])
+def test_djfa_step_hash_matches(vd, N, s, G):
+    # vd_djfa_step_hash: the checksum summed by the last pass (jump_pass_sk, N % 512 == 0, one band
+    # or banded) or by label_hash (N = 1000), equal to the oracle's label_hash of the new diagram
+    xy = synth.uniform_seeds(N, s, rng_seed=N + s)
+    d = _jfa_gpu(vd, N, xy, virtual_shards=G)
+    ref = oracle.jfa(N, xy)
+    out = torch.zeros(3, dtype=torch.int64).pin_memory()
+    want = []
+    for f in range(3):
+        disp = synth.displacements(s, 2, f, rng_seed=N)
+        vd.vd_djfa_step_hash(d.h, disp, 2, s, out[f].data_ptr())
+        ref, xy, _ = oracle.djfa_step(N, xy, disp, 2, ref)
+        want.append(oracle.label_hash(ref))
+    d.synchronize()
+    assert [int(v) & 0xFFFFFFFFFFFFFFFF for v in out] == want
+    assert np.array_equal(d.labels(), ref)
+
+
 # ---- packed-key passes (labels local to their pixels; vd_kernels.cuh row_packed) ---------
 # The kernel switches to the one-key evaluation when the kernel that wrote its input found
 # every label within distance 63 of its pixel (and k <= 64).  The result must not change:
