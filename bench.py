@@ -302,8 +302,11 @@ def run_gpu(args):
     e0, e1 = ev(), ev()
     with ClockSampler(local) as clk:
         e0.record(stream)
+        fev = [ev() for _ in range(K)] if args.frames_csv else None  # per-frame boundaries (optional CSV)
         for f in range(W, W + K):
             dj.djfa_step(disp_dev[f], d)
+            if fev:
+                fev[f - W].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -330,9 +333,12 @@ def run_gpu(args):
     jf.set_pass_timing(True)
     j0, j1 = ev(), ev()
     j0.record(stream)
+    jev = [ev() for _ in range(K)] if args.frames_csv else None
     for f in range(W, W + K):
         jf.move_seeds(disp_dev[f])
         jf.jfa()
+        if jev:
+            jev[f - W].record(stream)
     j1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -451,6 +457,22 @@ def run_gpu(args):
     pass_times = [(k, t) for k, t in dj_times if k != 0]
     fused = world == 1 and not remap_ms and pass_times
     first_k = pass_times[0][0] if fused else None
+    if args.frames_csv and rank == 0:  # one row per frame
+        import csv
+        with open(args.frames_csv, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["config", "n_gpus", "algorithm", "frame", "passes", "ms", "gpix_pass_per_s", "frac_hbm_measured",
+                        "frac_hbm_nominal"])
+            for name, starts, evs, npass in (("dJFA", e0, fev, passes), ("JFA", j0, jev, jpasses)):
+                prev = starts
+                for i, e in enumerate(evs):
+                    t = prev.elapsed_time(e)
+                    gbs = 8.0 * N * N * npass / (t / 1000.0) / 1e9
+                    w.writerow([args.config, world, name, W + i, npass, f"{t:.4f}",
+                                f"{N * N * npass / (t / 1000.0) / 1e9:.2f}", f"{gbs / peak:.4f}",
+                                f"{gbs / NOMINAL_HBM_GBS:.4f}"])
+                    prev = e
+
     dj_roof = roofline([(k, t) for k, t in pass_times if not fused or k != first_k], "jump_pass_sk (packed-key walk)")
     dj_roof["all_passes"] = {k: v for k, v in roofline(pass_times, "all jump passes of the frame").items()
                              if k in ("achieved", "frac", "frac_nominal", "avg_launch_ms", "launches_timed")}
@@ -521,6 +543,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--no-e2e-full", action="store_true", help="skip the e2e run that copies the whole map out")
+    ap.add_argument("--frames-csv", default=None, help="also write one CSV row per timed frame (dJFA and JFA)")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU oracle (cpu_baseline and parity)")
     ap.add_argument("--no-exact", action="store_true", help="skip the whole-grid similarity vs the exact diagram")
     ap.add_argument("--no-variants", action="store_true", help="skip the dJFAm (Manhattan) measurement")

@@ -28,7 +28,7 @@ tests) timeout 1500 python -m pytest tests -m "gpu and not slow" -x -q -p no:cac
 slowtests) timeout 2400 python -m pytest tests -m "gpu and slow" -x -q -p no:cacheprovider --durations=0 > gpurun_out/slowtests_$TAG.txt 2>&1; tail -30 gpurun_out/slowtests_$TAG.txt ;;
 alltests) timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider --durations=15 > gpurun_out/alltests_$TAG.txt 2>&1; tail -25 gpurun_out/alltests_$TAG.txt ;;
 smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 ;;
-bench) timeout 1200 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json ;;
+bench) timeout 1200 python bench.py --frames-csv gpurun_out/frames_$TAG.csv > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json ;;
 benchq) timeout 900 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-exact > gpurun_out/benchq_$TAG.json 2> gpurun_out/benchq_$TAG.err; tail -3 gpurun_out/benchq_$TAG.err; cat gpurun_out/benchq_$TAG.json ;;
 bench5) timeout 1500 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline --no-exact --no-variants --e2e-steps 3 > gpurun_out/bench5_$TAG.json 2> gpurun_out/bench5_$TAG.err; tail -3 gpurun_out/bench5_$TAG.err; cat gpurun_out/bench5_$TAG.json ;;
 ref) timeout 1200 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref_$TAG.json 2> gpurun_out/ref_$TAG.err; tail -3 gpurun_out/ref_$TAG.err; cat gpurun_out/ref_$TAG.json ;;
