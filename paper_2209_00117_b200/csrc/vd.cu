@@ -1318,22 +1318,19 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   if (st) return st;
   const int gs = grid_for(h, (int64_t)h->s, 256);
   // 1. SimulateParticles + forward map old -> new (R-9); fwd is all EMPTY on entry
-  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N);
-  if ((st = after_launch(h, "move_fwd"))) return st;
-  CK(cudaEventRecord(h->disp_used[slot], h->stream));
   const bool loc = loc_begin(h);
   // NEXT-1: on one band the first pass remaps its own staged rows (jump_pass_sk_remap): the
-  // new seed pixels are re-stamped first (flagged), the remapped diagram never goes to HBM,
-  // and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
+  // new seed pixels are re-stamped first (flagged, by move_fwd), the remapped diagram never goes
+  // to HBM, and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
   static const bool no_fuse = [] { const char* e = getenv("VD_NO_FUSE"); return e && e[0] == '1'; }();
   const uint32_t k1 = ks[0];
   const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->N <= 32768 &&
                     sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
+  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N,
+                                           fuse ? h->shards[0].buf[h->cur] : nullptr, h->pitch);
+  if ((st = after_launch(h, "move_fwd"))) return st;
+  CK(cudaEventRecord(h->disp_used[slot], h->stream));
   if (fuse) {
-    Shard& sh = h->shards[0];
-    vdk::stamp_flagged<<<gs, 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.row0, (int)sh.rows, h->seeds_new,
-                                                  (int64_t)h->s);
-    if ((st = after_launch(h, "stamp_flagged"))) return st;
     // Packed walk for the fused pass: every label of the previous diagram within kLocR of its
     // pixel (its flag, kLocPrev) and seeds that moved at most d_max per axis leave every remapped
     // label within kLocR + d_max*sqrt(2) of its pixel, so a candidate is within that + k1 per

@@ -849,7 +849,7 @@ __device__ __forceinline__ uint32_t min9_sk(const RowS<4 + 2 * KS>& A, const Row
 //
 // REMAP (NEXT-1, the first pass of a dJFA step, one band, stride steps 4 <= k <= 128): the
 // input holds the previous frame's labels, except the new seed pixels, which hold their new
-// label with bit 31 set (stamp_flagged).  Every slot label is remapped as the thread reads it
+// label with bit 31 set (stamped by move_fwd).  Every slot label is remapped as the thread reads it
 // from the stage -- labels[p] <- fwd[labels[p]] (Alg. 1's reuse of VD_{t-1}; R-9),
 // flagged labels unflagged -- so the remapped diagram is never written to HBM.  The gathers of
 // row j + 3 are issued while output row j is computed (one row of look-ahead), and neighbouring
@@ -1401,8 +1401,12 @@ __global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __r
 // new = clamp(old + disp) per axis (R-10; the reserved pixel at N = 65536, R-4), then
 // fwd[old] <- min(fwd[old], new): co-located seeds leave the smallest new label.  fwd is
 // all EMPTY between dJFA steps (reset_stamp restores it).
+// flag_g (or null): the fused frame (NEXT-1) also re-stamps the new seed pixel here, BEFORE the
+// first pass, with bit 31 set so that the pass's in-stage remap leaves it as it is (R-9: remap,
+// then re-stamp).  Labels are < 2^31 for N <= 32768, so the flag is free.  One band, rows [0, N).
 __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __restrict__ disp,
-                         uint32_t* __restrict__ new_s, uint32_t* __restrict__ fwd, int64_t s, int N) {
+                         uint32_t* __restrict__ new_s, uint32_t* __restrict__ fwd, int64_t s, int N,
+                         uint32_t* __restrict__ flag_g = nullptr, int64_t pitch = 0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t c = old_s[i];
     const short2 d = disp[i];
@@ -1413,6 +1417,7 @@ __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __res
     const uint32_t nw = ((uint32_t)y << 16) | (uint32_t)x;
     new_s[i] = nw;
     atomicMin(&fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)], nw);
+    if (flag_g) flag_g[(int64_t)y * pitch + x] = nw | 0x80000000u;
   }
 }
 
@@ -1433,19 +1438,8 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
   }
 }
 
-// Fused dJFA frame (NEXT-1): re-stamp the new seed pixels of this band BEFORE the first pass,
-// with bit 31 set so that the pass's in-stage remap leaves them as they are (R-9: remap, then
-// re-stamp).  Labels are < 2^31 (N <= 32768), so the flag is free.
-__global__ void stamp_flagged(uint32_t* __restrict__ g, int64_t pitch, int row0, int rows,
-                              const uint32_t* __restrict__ new_s, int64_t s) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = new_s[i];
-    const int y = (int)(c >> 16) - row0, x = (int)(c & 0xFFFFu);
-    if (y >= 0 && y < rows) g[(int64_t)y * pitch + x] = c | 0x80000000u;
-  }
-}
-
-// ... and after it: fwd back to all-EMPTY (its entries at the old seed pixels).
+// Fused dJFA frame (NEXT-1), after the first pass: fwd back to all-EMPTY (its entries at the old
+// seed pixels).
 __global__ void fwd_reset(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s, int64_t s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = old_s[i];
