@@ -490,18 +490,19 @@ bool encode_span_map(const vd_ctx* h, const uint32_t* in, uint32_t rows, uint32_
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int KM, bool ME, bool BD, bool HASH = false>
+template <int KM, bool ME, bool BD, bool HASH = false, int MINB = VD_MIN_BLOCKS>
 cudaError_t launch_sk(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk, size_t sm,
                       cudaStream_t st) {
   static std::atomic<uint64_t> opted{0};
   const uint64_t bit = 1ull << (dev & 63);
   if (!(opted.load(std::memory_order_acquire) & bit)) {
-    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk<KM, ME, BD, HASH>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, vdk::kSmemBudget);
+    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk<KM, ME, BD, HASH, MINB>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               MINB == 5 ? vdk::kSmemBudget5 : vdk::kSmemBudget);
     if (e != cudaSuccess) return e;
     opted.fetch_or(bit, std::memory_order_release);
   }
-  vdk::jump_pass_sk<KM, ME, BD, HASH><<<grid, blk, sm, st>>>(a, tm);
+  vdk::jump_pass_sk<KM, ME, BD, HASH, MINB><<<grid, blk, sm, st>>>(a, tm);
   return cudaSuccess;
 }
 template <int KM>
@@ -511,7 +512,7 @@ cudaError_t launch_sk_remap(int dev, const vdk::PassArgs& a, const CUtensorMap& 
   const uint64_t bit = 1ull << (dev & 63);
   if (!(opted.load(std::memory_order_acquire) & bit)) {
     const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk_remap<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               vdk::kSmemBudget);
+                                               vdk::kSmemBudget5);
     if (e != cudaSuccess) return e;
     opted.fetch_or(bit, std::memory_order_release);
   }
@@ -588,7 +589,11 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   if ((sk || fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, R);
     const uint32_t per_res = (R + k - 1) / k;
-    a.walk = sk ? vdk::walk_len_sk((int)k) : vdk::walk_len((int)k, rel);
+    // dJFA's stride passes (and its fused first pass) at five CTAs per SM with a 44-KB stage
+    static const bool no_five = [] { const char* e = getenv("VD_NO_FIVE"); return e && e[0] == '1'; }();
+    const bool five = sk && h->in_djfa && !may_empty && (h->fuse_remap || (!no_five && k >= 4 && k <= 64));
+    const int budget = five ? vdk::kSmemBudget5 : vdk::kSmemBudget;
+    a.walk = sk ? vdk::walk_len_sk((int)k, budget) : vdk::walk_len((int)k, rel);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     // Small grids (C2: 1024^2 at k = 1 is 2 x 1 x 43 walks of 24 rows): shorten the walks until
     // there are about two waves of resident CTAs, else a few long walks leave SMs idle.
@@ -639,7 +644,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     } else {
       h->pass_loc_ok = false;
     }
-    const size_t sm = sk ? vdk::pass_smem_sk((int)k) : vdk::pass_smem((int)k, rel);
+    const size_t sm = sk ? vdk::pass_smem_sk((int)k, budget) : vdk::pass_smem((int)k, rel);
     cudaError_t e;
     if (sk) {
       // k >= 256 on one band: one tensor copy per staged row (VD_NO_TMAP=1: six bulk copies)
@@ -675,11 +680,31 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
           }
           break;
         case 2: e = launch_sk_k<2>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 4: e = launch_sk_k<4>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 8: e = launch_sk_k<8>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 16: e = launch_sk_k<16>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 32: e = launch_sk_k<32>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 64: e = launch_sk_k<64>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        case 4:
+          e = five ? (banded ? launch_sk<4, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
+                             : launch_sk<4, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
+                   : launch_sk_k<4>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+          break;
+        case 8:
+          e = five ? (banded ? launch_sk<8, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
+                             : launch_sk<8, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
+                   : launch_sk_k<8>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+          break;
+        case 16:
+          e = five ? (banded ? launch_sk<16, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
+                             : launch_sk<16, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
+                   : launch_sk_k<16>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+          break;
+        case 32:
+          e = five ? (banded ? launch_sk<32, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
+                             : launch_sk<32, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
+                   : launch_sk_k<32>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+          break;
+        case 64:
+          e = five ? (banded ? launch_sk<64, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
+                             : launch_sk<64, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
+                   : launch_sk_k<64>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+          break;
         case 128: e = launch_sk_k<128>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 256: e = launch_sk_k<256>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
         case 512: e = launch_sk_k<512>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;

@@ -732,12 +732,19 @@ struct RowS {
 };
 
 __host__ __device__ inline int stage_elems_sk(int k) { return k >= 256 ? 6 * 128 : stage_elems(k); }
-__host__ __device__ inline int walk_len_sk(int k) {
-  const int rows = kSmemBudget / (stage_elems_sk(k) * 4 + 8);
+// Five CTAs per SM (dJFA's stride passes, 4 <= k <= 64, and the fused first pass): <= 102
+// registers and a 44-KB stage, measured 2.5-5% faster than four CTAs with 56 KB for those passes
+// (and slower for the exact walk of JFA and for k <= 2, which keep four).
+#ifndef VD_SMEM_KB5
+#define VD_SMEM_KB5 44
+#endif
+constexpr int kSmemBudget5 = VD_SMEM_KB5 * 1024;
+__host__ __device__ inline int walk_len_sk(int k, int budget = kSmemBudget) {
+  const int rows = budget / (stage_elems_sk(k) * 4 + 8);
   return rows - 2 < 1 ? 1 : (rows - 2 > kMaxWalk ? kMaxWalk : rows - 2);
 }
-__host__ __device__ inline size_t pass_smem_sk(int k) {
-  return (size_t)(walk_len_sk(k) + 2) * (stage_elems_sk(k) * 4 + 8);
+__host__ __device__ inline size_t pass_smem_sk(int k, int budget = kSmemBudget) {
+  return (size_t)(walk_len_sk(k, budget) + 2) * (stage_elems_sk(k) * 4 + 8);
 }
 
 // Row build from the NS slot labels.  xs_home[s]: -(column of slot s) << 16 (+1 for PACK);
@@ -1134,8 +1141,8 @@ __host__ __device__ constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2
 // groups of a.nwalk residue classes.  Host: N % 512 == 0, k a power of two, k <= N / 4;
 // Euclidean Moore passes, no window (N <= 32768).  KM: k itself for k <= 4096 (compile-time
 // step), 8192 for any larger k.
-template <int KM, bool MAY_EMPTY, bool BANDED, bool HASH = false>
-__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
+template <int KM, bool MAY_EMPTY, bool BANDED, bool HASH = false, int MINB = VD_MIN_BLOCKS>
+__global__ void __launch_bounds__(kThreads, MINB) jump_pass_sk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)blockIdx.x;
   const bool full = a.nwalk > 0;
@@ -1187,7 +1194,7 @@ __global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk(PassArgs
 // The first pass of a dJFA step with the remap fused in (walk_sk REMAP): one band, stride steps
 // 4 <= k <= 128.
 template <int KM>
-__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_sk_remap(PassArgs a, const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(kThreads, 5) jump_pass_sk_remap(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
   const int xb = (int)blockIdx.x;
   const int seg = (int)(a.res_in_y ? blockIdx.z : blockIdx.y), res = (int)(a.res_in_y ? blockIdx.y : blockIdx.z);

@@ -702,7 +702,7 @@ def test_packed_passes_ragged_grid_bit_exact(vd, N):
 
 
 @pytest.mark.parametrize("env", ["VD_NO_FIRST_SCATTER=1", "VD_NO_SK=1", "VD_NO_FULL=1", "VD_ORDER=1", "VD_NO_FUSE=1",
-                                 "VD_REMAP=1", "VD_NO_TMAP=1"])
+                                 "VD_REMAP=1", "VD_NO_TMAP=1", "VD_NO_FIVE=1", "VD_FUSE_PF=0"])
 def test_kernel_variant_switches_bit_exact(vd, env):
     # The A/B switches (read once per process) select the r01 kernels: JFA's init + gather
     # first pass instead of the seed scatter, jump_pass_fast instead of jump_pass_sk, segment
