@@ -26,6 +26,7 @@
 
 #include "../../include/vd.h"
 #include "vd_kernels.cuh"
+#include "vd_launch.h"
 
 namespace {
 
@@ -406,46 +407,6 @@ vd_status timed_end(vd_ctx* h, uint64_t px, uint32_t k) {
   return VD_OK;
 }
 
-// Which kernel variant can take this pass exactly (see vd_kernels.cuh).
-// Launch one fast-pass instantiation; each opts into the largest staging size once.
-// The dynamic shared-memory opt-in is a per-device function attribute: set it once per
-// (instantiation, device), remembered in a per-instantiation device bitmask (a concurrent
-// first use on two threads sets the same value twice, which is harmless).
-template <int KM, bool ME, bool BD, int MT, bool VN, bool REL>
-cudaError_t launch_fast(int dev, const vdk::PassArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t st) {
-  static std::atomic<uint64_t> opted{0};
-  const uint64_t bit = 1ull << (dev & 63);
-  if (!(opted.load(std::memory_order_acquire) & bit)) {
-    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               REL ? vdk::kSmemBudgetRel : vdk::kSmemBudget);
-    if (e != cudaSuccess) return e;
-    opted.fetch_or(bit, std::memory_order_release);
-  }
-  vdk::jump_pass_fast<KM, ME, BD, MT, VN, REL><<<grid, blk, sm, st>>>(a);
-  return cudaSuccess;
-}
-template <int KM, bool ME, bool BD, bool REL>
-cudaError_t launch_fast_mv(int dev, int metric, bool vn, const vdk::PassArgs& a, dim3 g, dim3 b, size_t sm,
-                           cudaStream_t st) {
-  if (metric == 0)
-    return vn ? launch_fast<KM, ME, BD, 0, true, REL>(dev, a, g, b, sm, st)
-              : launch_fast<KM, ME, BD, 0, false, REL>(dev, a, g, b, sm, st);
-  return vn ? launch_fast<KM, ME, BD, 1, true, REL>(dev, a, g, b, sm, st)
-            : launch_fast<KM, ME, BD, 1, false, REL>(dev, a, g, b, sm, st);
-}
-template <int KM>
-cudaError_t launch_fast_k(int dev, bool me, bool bd, bool rel, int metric, bool vn, const vdk::PassArgs& a, dim3 g,
-                          dim3 b, size_t sm, cudaStream_t st) {
-  if (rel)  // windowed coordinates (complete diagrams beyond the plain fast kernel's range)
-    return bd ? launch_fast_mv<KM, false, true, true>(dev, metric, vn, a, g, b, sm, st)
-              : launch_fast_mv<KM, false, false, true>(dev, metric, vn, a, g, b, sm, st);
-  if (me) return bd ? launch_fast_mv<KM, true, true, false>(dev, metric, vn, a, g, b, sm, st)
-                    : launch_fast_mv<KM, true, false, false>(dev, metric, vn, a, g, b, sm, st);
-  return bd ? launch_fast_mv<KM, false, true, false>(dev, metric, vn, a, g, b, sm, st)
-            : launch_fast_mv<KM, false, false, false>(dev, metric, vn, a, g, b, sm, st);
-}
-
 // Shared-term kernel (jump_pass_sk): one band or banded, Euclidean Moore, N % 512 == 0, and
 // k in {1, 2} (adjacent columns) or 32 <= k <= N/4 (stride columns).  VD_NO_SK=1 disables it
 // (A/B timing).
@@ -488,43 +449,6 @@ bool encode_span_map(const vd_ctx* h, const uint32_t* in, uint32_t rows, uint32_
   return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(in), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-template <int KM, bool ME, bool BD, bool HASH = false, int MINB = VD_MIN_BLOCKS>
-cudaError_t launch_sk(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk, size_t sm,
-                      cudaStream_t st) {
-  static std::atomic<uint64_t> opted{0};
-  const uint64_t bit = 1ull << (dev & 63);
-  if (!(opted.load(std::memory_order_acquire) & bit)) {
-    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk<KM, ME, BD, HASH, MINB>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               MINB == 5 ? vdk::kSmemBudget5 : vdk::kSmemBudget);
-    if (e != cudaSuccess) return e;
-    opted.fetch_or(bit, std::memory_order_release);
-  }
-  vdk::jump_pass_sk<KM, ME, BD, HASH, MINB><<<grid, blk, sm, st>>>(a, tm);
-  return cudaSuccess;
-}
-template <int KM>
-cudaError_t launch_sk_remap(int dev, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk, size_t sm,
-                            cudaStream_t st) {
-  static std::atomic<uint64_t> opted{0};
-  const uint64_t bit = 1ull << (dev & 63);
-  if (!(opted.load(std::memory_order_acquire) & bit)) {
-    const cudaError_t e = cudaFuncSetAttribute(vdk::jump_pass_sk_remap<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               vdk::kSmemBudget5);
-    if (e != cudaSuccess) return e;
-    opted.fetch_or(bit, std::memory_order_release);
-  }
-  vdk::jump_pass_sk_remap<KM><<<grid, blk, sm, st>>>(a, tm);
-  return cudaSuccess;
-}
-
-template <int KM>
-cudaError_t launch_sk_k(int dev, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 g, dim3 b,
-                        size_t sm, cudaStream_t st) {
-  if (me) return bd ? launch_sk<KM, true, true>(dev, a, tm, g, b, sm, st) : launch_sk<KM, true, false>(dev, a, tm, g, b, sm, st);
-  return bd ? launch_sk<KM, false, true>(dev, a, tm, g, b, sm, st) : launch_sk<KM, false, false>(dev, a, tm, g, b, sm, st);
 }
 
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
@@ -660,62 +584,14 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
         a.loc_in = h->pass_loc_in;  // the previous frame's locality, when the moves keep the packed key valid
         a.nwalk = 0;
         const dim3 g2((unsigned)a.xblocks, a.res_in_y ? nres : (unsigned)a.segs, a.res_in_y ? (unsigned)a.segs : nres);
-        switch (k) {
-          case 4: e = launch_sk_remap<4>(h->device, a, tm, g2, blk, sm, h->stream); break;
-          case 8: e = launch_sk_remap<8>(h->device, a, tm, g2, blk, sm, h->stream); break;
-          case 16: e = launch_sk_remap<16>(h->device, a, tm, g2, blk, sm, h->stream); break;
-          case 32: e = launch_sk_remap<32>(h->device, a, tm, g2, blk, sm, h->stream); break;
-          case 64: e = launch_sk_remap<64>(h->device, a, tm, g2, blk, sm, h->stream); break;
-          default: e = launch_sk_remap<128>(h->device, a, tm, g2, blk, sm, h->stream); break;
-        }
-      } else
-      switch (k) {
-        case 1:
-          if (h->hash_pass && !may_empty) {  // the frame's last pass also sums the label checksum
-            a.hash_out = h->counter;
-            e = banded ? launch_sk<1, false, true, true>(h->device, a, tm, grid, blk, sm, h->stream)
-                       : launch_sk<1, false, false, true>(h->device, a, tm, grid, blk, sm, h->stream);
-          } else {
-            e = launch_sk_k<1>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
-          }
-          break;
-        case 2: e = launch_sk_k<2>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 4:
-          e = five ? (banded ? launch_sk<4, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
-                             : launch_sk<4, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
-                   : launch_sk_k<4>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
-          break;
-        case 8:
-          e = five ? (banded ? launch_sk<8, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
-                             : launch_sk<8, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
-                   : launch_sk_k<8>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
-          break;
-        case 16:
-          e = five ? (banded ? launch_sk<16, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
-                             : launch_sk<16, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
-                   : launch_sk_k<16>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
-          break;
-        case 32:
-          e = five ? (banded ? launch_sk<32, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
-                             : launch_sk<32, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
-                   : launch_sk_k<32>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
-          break;
-        case 64:
-          e = five ? (banded ? launch_sk<64, false, true, false, 5>(h->device, a, tm, grid, blk, sm, h->stream)
-                             : launch_sk<64, false, false, false, 5>(h->device, a, tm, grid, blk, sm, h->stream))
-                   : launch_sk_k<64>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
-          break;
-        case 128: e = launch_sk_k<128>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 256: e = launch_sk_k<256>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 512: e = launch_sk_k<512>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 1024: e = launch_sk_k<1024>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 2048: e = launch_sk_k<2048>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        case 4096: e = launch_sk_k<4096>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
-        default: e = launch_sk_k<8192>(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream); break;
+        e = vdl::launch_sk_remap(h->device, k, a, tm, g2, blk, sm, h->stream);
+      } else {
+        if (k == 1 && h->hash_pass && !may_empty) a.hash_out = h->counter;  // the frame's last pass also sums the checksum
+        e = vdl::launch_sk(h->device, k, may_empty, banded, five, a.hash_out != nullptr, a, tm, grid, blk, sm, h->stream);
       }
-    } else if (k == 1) e = launch_fast_k<1>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
-    else if (k == 2) e = launch_fast_k<2>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
-    else e = launch_fast_k<4>(h->device, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    } else {
+      e = vdl::launch_fast(h->device, k, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
+    }
     CK(e);
   } else {
     h->pass_loc_ok = false;  // the wide kernel does not report locality
@@ -724,18 +600,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     a.walk = 1;
     const int64_t blocks = (int64_t)a.xblocks * nres * a.segs;
     const dim3 g((unsigned)blocks), b(vdk::kThreads);
-    const bool v4 = (k % 4) == 0;
-    if (h->metric == 0) {
-      if (vn) v4 ? vdk::jump_pass_wide<0, true, true><<<g, b, 0, h->stream>>>(a)
-              : vdk::jump_pass_wide<0, true, false><<<g, b, 0, h->stream>>>(a);
-      else v4 ? vdk::jump_pass_wide<0, false, true><<<g, b, 0, h->stream>>>(a)
-              : vdk::jump_pass_wide<0, false, false><<<g, b, 0, h->stream>>>(a);
-    } else {
-      if (vn) v4 ? vdk::jump_pass_wide<1, true, true><<<g, b, 0, h->stream>>>(a)
-              : vdk::jump_pass_wide<1, true, false><<<g, b, 0, h->stream>>>(a);
-      else v4 ? vdk::jump_pass_wide<1, false, true><<<g, b, 0, h->stream>>>(a)
-              : vdk::jump_pass_wide<1, false, false><<<g, b, 0, h->stream>>>(a);
-    }
+    CK(vdl::launch_wide(k, h->metric, vn, a, g, b, h->stream));
   }
   return after_launch(h, "jump_pass");
 }

@@ -1273,6 +1273,7 @@ __global__ void __launch_bounds__(kThreads) jump_pass_wide(PassArgs a) {
   if (a.empty_flag != nullptr && __syncthreads_or(any_empty) && threadIdx.x == 0) atomicOr(a.empty_flag, 1ull);
 }
 
+#ifndef VD_TEMPLATE_KERNELS_ONLY  // the non-template kernels live in vd.cu's translation unit only
 // ------------------------------------------------------------------ peer halos (NEXT-3)
 // Copy this band's first / last k rows into the neighbours' halo buffers (the first pass of
 // a sequence; later passes push from inside the pass kernel, store_out).
@@ -1618,5 +1619,7 @@ __global__ void label_hash(const uint32_t* __restrict__ g, int64_t pitch, int ro
   uint64_t t = block_sum_u64(h);
   if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)t);
 }
+
+#endif  // VD_TEMPLATE_KERNELS_ONLY
 
 }  // namespace vdk
