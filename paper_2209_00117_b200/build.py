@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 # kernel family (vd_launch_*.cu), compiled in parallel and linked into one shared library
 SRC = [os.path.join(PKG, "csrc", f) for f in ("vd.cu", "vd_launch_sk_small.cu", "vd_launch_sk_mid.cu",
                                                "vd_launch_sk_large.cu", "vd_launch_remap.cu", "vd_launch_fast.cu",
-                                               "vd_launch_wide.cu")]
+                                               "vd_launch_wide.cu", "vd_launch_wsk.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "vd_kernels.cuh"), os.path.join(PKG, "csrc", "vd_launch.h"),
               os.path.join(ROOT, "include", "vd.h")]
 LIB = os.path.join(PKG, "libvd.so")

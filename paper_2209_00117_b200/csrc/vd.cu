@@ -451,6 +451,15 @@ bool encode_span_map(const vd_ctx* h, const uint32_t* in, uint32_t rows, uint32_
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Wide exact pass (jump_pass_wsk): grids beyond N = 32768 (33-bit squared distances), any labels,
+// EMPTY allowed, Euclidean Moore, power-of-two 256 <= k <= N / 4, N % 512 == 0 (JFA's large steps
+// at C5).  VD_NO_WSK=1 disables it (A/B against the windowed / 64-bit kernels).
+bool wsk_ok(const vd_ctx* h, uint32_t k, bool vn) {
+  static const bool off = [] { const char* e = getenv("VD_NO_WSK"); return e && e[0] == '1'; }();
+  return !off && !h->force_rel && h->N > 32768 && h->N % 512 == 0 && h->metric == 0 && !vn && k >= 256 &&
+         (k & (k - 1)) == 0 && 4 * k <= h->N;
+}
+
 bool fast_ok(uint32_t N, bool may_empty) { return may_empty ? N <= 16384 : N <= 32768; }
 // Windowed fast pass (REL) for complete diagrams with 32768 < N <= 65536 and steps small
 // enough that a walk and its neighbour rows fit the 32768-wide window (dJFA's delta passes,
@@ -509,15 +518,16 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   const uint32_t R = (uint32_t)(y_hi - y_lo);  // output rows of this launch
   if (R == 0) return VD_OK;
   const bool sk = sk_ok(h, k, vn, may_empty) && (k & (k - 1)) == 0;
-  const bool rel = !sk && (rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096));
-  if ((sk || fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
+  const bool wsk = !sk && wsk_ok(h, k, vn);
+  const bool rel = !sk && !wsk && (rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096));
+  if ((sk || wsk || fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
     const uint32_t nres = std::min(k, R);
     const uint32_t per_res = (R + k - 1) / k;
     // dJFA's stride passes (and its fused first pass) at five CTAs per SM with a 44-KB stage
     static const bool no_five = [] { const char* e = getenv("VD_NO_FIVE"); return e && e[0] == '1'; }();
     const bool five = sk && h->in_djfa && !may_empty && (h->fuse_remap || (!no_five && k >= 4 && k <= 64));
     const int budget = five ? vdk::kSmemBudget5 : vdk::kSmemBudget;
-    a.walk = sk ? vdk::walk_len_sk((int)k, budget) : vdk::walk_len((int)k, rel);
+    a.walk = sk || wsk ? vdk::walk_len_sk((int)k, budget) : vdk::walk_len((int)k, rel);
     if (rel) a.walk = std::max(1, std::min(a.walk, (int)(8192 / k) + 1));  // walk span <= 8192 rows
     // Small grids (C2: 1024^2 at k = 1 is 2 x 1 x 43 walks of 24 rows): shorten the walks until
     // there are about two waves of resident CTAs, else a few long walks leave SMs idle.
@@ -543,7 +553,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     const bool banded = sh.top[0] != nullptr;
     a.nwalk = 0;
     unsigned gz = a.res_in_y ? (unsigned)a.segs : nres, gy = a.res_in_y ? nres : (unsigned)a.segs;
-    if (sk && !h->fuse_remap && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
+    if ((sk || wsk) && !h->fuse_remap && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
       const uint32_t per = h->N / k, fit = (uint32_t)vdk::walk_len_sk((int)k) + 2;
       if (4 * per <= fit) {  // (one or two classes per CTA measured slower than segment walks)
         // as many classes per CTA as fit, but keep >= 4 CTAs per SM in the grid
@@ -556,7 +566,11 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
         gz = (k + (uint32_t)a.nwalk - 1) / (uint32_t)a.nwalk;
       }
     }
-    const dim3 grid((unsigned)a.xblocks, gy, gz), blk(vdk::kThreads);
+    // spans (k >= 256): groups of 4k columns, k / 128 CTAs each; the last group is partial when
+    // 4k does not divide N
+    const unsigned gx = (sk || wsk) && k >= 256 ? (unsigned)(((h->N + 4 * k - 1) / (4 * k)) * (k / 128))
+                                                : (unsigned)a.xblocks;
+    const dim3 grid(gx, gy, gz), blk(vdk::kThreads);
     // locality (the kernels' LOC variants: Euclidean Moore).  A launch whose rows read halo
     // rows (written by other bands, whose locality this band's flag does not cover) keeps
     // the exact walk; the interior launch of an overlapped sharded pass reads none.
@@ -568,16 +582,19 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     } else {
       h->pass_loc_ok = false;
     }
-    const size_t sm = sk ? vdk::pass_smem_sk((int)k, budget) : vdk::pass_smem((int)k, rel);
+    const size_t sm = sk || wsk ? vdk::pass_smem_sk((int)k, budget) : vdk::pass_smem((int)k, rel);
     cudaError_t e;
-    if (sk) {
+    if (sk || wsk) {
       // k >= 256 on one band: one tensor copy per staged row (VD_NO_TMAP=1: six bulk copies)
       static const bool no_tmap = [] { const char* e = getenv("VD_NO_TMAP"); return e && e[0] == '1'; }();
       CUtensorMap tm;
       memset(&tm, 0, sizeof tm);
       a.tmap = 0;
-      if (k >= 256 && !banded && !no_tmap && encode_span_map(h, a.in, sh.rows, k, &tm)) a.tmap = 1;
-      if (h->fuse_remap) {  // first dJFA pass with the remap fused in (vd_djfa_step checked the conditions)
+      // (the row viewed as [N/k][k]: needs k | N)
+      if (k >= 256 && h->N % k == 0 && !banded && !no_tmap && encode_span_map(h, a.in, sh.rows, k, &tm)) a.tmap = 1;
+      if (wsk) {
+        e = vdl::launch_wsk(h->device, may_empty, banded, a, tm, grid, blk, sm, h->stream);
+      } else if (h->fuse_remap) {  // first dJFA pass with the remap fused in (vd_djfa_step checked the conditions)
         a.fwd = h->fwd;
         static const int pf = [] { const char* e = getenv("VD_FUSE_PF"); return e ? atoi(e) : 1; }();
         a.prefetch = pf;
@@ -1111,7 +1128,7 @@ vd_status vd_jfa(vd_handle h) {
     }
     // JFA's labels are still far from their pixels at large steps: there the windowed kernel
     // would recompute most walks, and the 64-bit one is cheaper (C5: 31 vs 68 ms at k = 512).
-    const bool far = h->N > 32768 && ks[i] > 256;
+    const bool far = h->N > 32768 && ks[i] > 256 && !wsk_ok(h, ks[i], vn);
     st = run_pass(h, ks[i], may_empty || far, vn, i + 1 < ks.size() ? ks[i + 1] : 0);
     h->track_empty = false;
     if (st) return loc_end(h), st;
@@ -1210,11 +1227,11 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   // 1. SimulateParticles + forward map old -> new (R-9); fwd is all EMPTY on entry
   const bool loc = loc_begin(h);
   // NEXT-1: on one band the first pass remaps its own staged rows (jump_pass_sk_remap): the
-  // new seed pixels are re-stamped first (flagged, by move_fwd), the remapped diagram never goes
-  // to HBM, and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
+  // new seed pixels are marked first (EMPTY, by move_fwd), the remapped diagram never goes to HBM,
+  // and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
   static const bool no_fuse = [] { const char* e = getenv("VD_NO_FUSE"); return e && e[0] == '1'; }();
   const uint32_t k1 = ks[0];
-  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->N <= 32768 &&
+  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 &&
                     sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
   vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N,
                                            fuse ? h->shards[0].buf[h->cur] : nullptr, h->pitch);

@@ -855,10 +855,11 @@ __device__ __forceinline__ uint32_t min9_sk(const RowS<4 + 2 * KS>& A, const Row
 // runs one walk segment of a.walk rows starting at y0, as jump_pass_fast.
 //
 // REMAP (NEXT-1, the first pass of a dJFA step, one band, stride steps 4 <= k <= 128): the
-// input holds the previous frame's labels, except the new seed pixels, which hold their new
-// label with bit 31 set (stamped by move_fwd).  Every slot label is remapped as the thread reads it
-// from the stage -- labels[p] <- fwd[labels[p]] (Alg. 1's reuse of VD_{t-1}; R-9),
-// flagged labels unflagged -- so the remapped diagram is never written to HBM.  The gathers of
+// input holds the previous frame's labels, except the new seed pixels, which hold the marker EMPTY
+// (written by move_fwd; a dJFA diagram is complete, so EMPTY is free at every N, 65536 included).
+// Every slot label is remapped as the thread reads it from the stage -- labels[p] <- fwd[labels[p]]
+// (Alg. 1's reuse of VD_{t-1}; R-9), a marker becomes the pixel's own position (the
+// re-stamp) -- so the remapped diagram is never written to HBM.  The gathers of
 // row j + 3 are issued while output row j is computed (one row of look-ahead), and neighbouring
 // lanes mostly ask for the same fwd entry, which the L1 serves once per warp instruction.
 // X64 (grids beyond N = 32768, whose labels are not all local): the same walk with the exact key
@@ -879,30 +880,15 @@ __device__ __forceinline__ uint32_t best64_sk(const RowS<4 + 2 * KS>& A, const R
   return bc;
 }
 
-// HASH (the last pass of an e2e dJFA step, KM = 1): every output label is also added to the
-// frame's checksum, sum over p of fmix32((y N + x) * 0x9E3779B9 ^ label) mod 2^64 (label_hash),
-// so the step needs no separate 4-B/px read for its result.
-template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false,
-          bool X64 = false, bool HASH = false>
-__device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
-                                        uint32_t* smem) {
-  constexpr int KS = KM < kVec ? KM : 1;
-  constexpr int NS = 4 + 2 * KS;
-  constexpr bool STRIDE = KM >= kVec;
-  constexpr int KC = (STRIDE && KM <= 4096) ? KM : 0;  // compile-time step: immediate offsets
-  const int k = KC ? KC : a.k, N = a.N;
-  const int tid = (int)threadIdx.x;
-  // FULL: walks y0 + w (w < nw), each of nout rows; stage slot of (walk w, row j) = w * nout + j.
-  // Else: one walk; stage slot i = logical row i (0 = the row above the first output row).
-  const int nw = FULL ? min(a.nwalk, k - (y0 - a.y_lo)) : 1;
-  const int nout = FULL ? (a.y_hi - y0 + k - 1) >> a.lk : min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
-  const int nlist = FULL ? nw * nout : nout + 2;
-  const bool spans = STRIDE && k >= 256;
-  const int K4 = (k + 3) & ~3;
-  const int SE = stage_elems_sk(k);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
-
-  if constexpr (!PRE) {
+// Stage every input row of a walk (walk_sk, walk_wsk) into shared memory: one mbarrier per row,
+// warp w issues the copies of rows w, w + 4, ... (one elected lane).  FULL: a.nwalk whole residue
+// classes (y0 + w), stage slot w * nout + j = row y0 + w + j k; else one walk segment, slot i = row
+// y0 + (i - 1) k, rows outside the grid replaced by the centre row.  spans (k >= 256): six
+// 128-column spans x0 + j k (j = -1..4) per row, with one tensor copy when a.tmap.
+template <bool FULL, bool BANDED>
+__device__ __forceinline__ void stage_walk(const PassArgs& a, const CUtensorMap* tm, int x0, int y0, int k, int nout,
+                                           int nlist, bool spans, int K4, int SE, uint32_t* smem, uint64_t* bars) {
+  const int tid = (int)threadIdx.x, N = a.N;
   for (int i = tid; i < nlist; i += kThreads) mbar_init(&bars[i], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -951,7 +937,32 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       __syncwarp();
     }
   }
-  }  // !PRE
+}
+
+// HASH (the last pass of an e2e dJFA step, KM = 1): every output label is also added to the
+// frame's checksum, sum over p of fmix32((y N + x) * 0x9E3779B9 ^ label) mod 2^64 (label_hash),
+// so the step needs no separate 4-B/px read for its result.
+template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false,
+          bool X64 = false, bool HASH = false>
+__device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
+                                        uint32_t* smem) {
+  constexpr int KS = KM < kVec ? KM : 1;
+  constexpr int NS = 4 + 2 * KS;
+  constexpr bool STRIDE = KM >= kVec;
+  constexpr int KC = (STRIDE && KM <= 4096) ? KM : 0;  // compile-time step: immediate offsets
+  const int k = KC ? KC : a.k, N = a.N;
+  const int tid = (int)threadIdx.x;
+  // FULL: walks y0 + w (w < nw), each of nout rows; stage slot of (walk w, row j) = w * nout + j.
+  // Else: one walk; stage slot i = logical row i (0 = the row above the first output row).
+  const int nw = FULL ? min(a.nwalk, k - (y0 - a.y_lo)) : 1;
+  const int nout = FULL ? (a.y_hi - y0 + k - 1) >> a.lk : min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
+  const int nlist = FULL ? nw * nout : nout + 2;
+  const bool spans = STRIDE && k >= 256;
+  const int K4 = (k + 3) & ~3;
+  const int SE = stage_elems_sk(k);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
+
+  if constexpr (!PRE) stage_walk<FULL, BANDED>(a, tm, x0, y0, k, nout, nlist, spans, K4, SE, smem, bars);
 
   // per-thread slot offsets in a stage, columns, and edge flags
   const uint32_t sh16 = a.sh16;
@@ -966,6 +977,10 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   for (int e = 0; e < kVec; ++e) xs_out[e] = (int)(P1 - ((uint32_t)(STRIDE ? X + e * k : X + e) << 16));
   const bool left_out = FIX && (STRIDE ? X - k < 0 : X - KS < 0);
   const bool right_out = FIX && (STRIDE ? X + 4 * k >= N : X + 3 + KS >= N);
+  // stride: slot s (column X + (s-1) k) lies in the grid iff s - 1 < nc, output e iff e < nc.  With
+  // spans (k >= 256) on a grid that is not a multiple of 4k the last group of 4k columns is partial:
+  // there nc < 4 (outputs beyond the grid are not stored, slots beyond it duplicate their left slot)
+  const int nc = (STRIDE && FIX) ? (X >= N ? 0 : ((N - 1 - X) >> a.lk) + 1) : 8;
   int xb[kVec];
 #pragma unroll
   for (int e = 0; e < kVec; ++e) xb[e] = (STRIDE ? X + e * k : X + e) - 128;
@@ -992,10 +1007,20 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
 #pragma unroll
       for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
     }
+    // a new seed pixel holds the marker EMPTY (move_fwd; a dJFA diagram has no EMPTY): its label is
+    // its own position -- the row of stage slot i (rows outside the grid were staged as the centre
+    // row) and the slot's column (an out-of-grid slot holds its in-grid duplicate's label)
+    int r = y0 + (i - 1) * k;
+    if (r < 0) r += k;
+    else if (r >= N) r -= k;
+    const uint32_t own0 = ((uint32_t)r << 16) + (uint32_t)(X - k);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const uint32_t c = lab[s];
-      lab[s] = (c & 0x80000000u) ? (c ^ 0x80000000u) : __ldg(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu)));
+      uint32_t own = own0 + (uint32_t)(s * k);
+      if (FIX && s == 0 && left_out) own += (uint32_t)k;
+      if (FIX && s == NS - 1 && right_out) own -= (uint32_t)k;
+      lab[s] = c == EMPTY ? own : __ldg(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu)));
     }
   };
   auto consume = [&](int i, R_t& R) {
@@ -1016,8 +1041,13 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
     if constexpr (FIX) {  // out-of-grid neighbour -> the same output's centre label (a duplicate)
 #pragma unroll
       for (int s = 0; s < KS; ++s) lab[s] = left_out ? lab[s + KS] : lab[s];
+      if constexpr (STRIDE) {
 #pragma unroll
-      for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
+        for (int s = 1; s < NS; ++s) lab[s] = s >= nc + 1 ? lab[s - 1] : lab[s];
+      } else {
+#pragma unroll
+        for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
+      }
     }
     build_sk<KS, MAY_EMPTY, PACK>(lab, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, R);
   };
@@ -1056,7 +1086,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
 #pragma unroll
           for (int s = 0; s < NS; ++s) {
             const uint32_t c = st[sbase + s * (spans ? 128 : k)];
-            if (!(c & 0x80000000u))
+            if (c != EMPTY)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu))));
           }
         }
@@ -1104,7 +1134,8 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         store_out(a, BANDED, y, X, po, make_uint4(o[0], o[1], o[2], o[3]));
       } else {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) store_out(a, BANDED, y, X + e * k, po + e * k, o[e]);
+        for (int e = 0; e < kVec; ++e)
+          if (e < nc) store_out(a, BANDED, y, X + e * k, po + e * k, o[e]);
       }
       po += kp;
       y += k;
@@ -1166,7 +1197,8 @@ __global__ void __launch_bounds__(kThreads, MINB) jump_pass_sk(PassArgs a, const
     const int g = xb >> lr, rb = xb & ((1 << lr) - 1);
     x0 = 4 * k * g + 128 * rb;
     X = x0 + tid;
-    fix = g == 0 || x0 - 128 * rb + 4 * k >= a.N;
+    fix = g == 0 || x0 + 4 * k + 128 > a.N;  // some right neighbour column (X + 4k) beyond the grid
+    if (x0 >= a.N) return;  // (the partial last group of a grid that is not a multiple of 4k)
   }
   if (full) {  // JFA's large steps: exact walk (their diagrams are never local)
     if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, true, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);
@@ -1211,8 +1243,249 @@ __global__ void __launch_bounds__(kThreads, 5) jump_pass_sk_remap(PassArgs a, co
     else walk_sk<KM, false, false, false, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
     return;
   }
+  if (a.N > 32768) {  // 32-bit squared distances would overflow: exact 64-bit keys (X64)
+    if (fix) walk_sk<KM, false, false, true, false, false, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    else walk_sk<KM, false, false, false, false, false, true, false, true>(a, &tm, x0, X, y0, dyn_smem);
+    return;
+  }
   if (fix) walk_sk<KM, false, false, true, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
   else walk_sk<KM, false, false, false, false, false, true>(a, &tm, x0, X, y0, dyn_smem);
+}
+
+// ------------------------------------------------------------------ wide exact pass (r02: N <= 65536)
+//
+// The exact pass (key (d2, c) lexicographically, R-3) for grids beyond N = 32768, whose
+// squared distances need 33 bits, with EMPTY allowed: JFA's large steps at C5, where labels are far
+// from their pixels (jump_pass_wide did these with per-candidate 64-bit compares, ~200 instructions
+// per pixel).  Stride layout with spans (k >= 256, power of two, 4k <= N, N % 512 == 0) and the
+// staging of walk_sk; one thread = output columns Xo_e = X + e k (e = 0..3) of each output row.
+//
+// Per output row y let h = y >> 1 and p = y & 1 (p is the same for every row of a walk, k even).
+// For a label c = (cy, cx) and output column Xo, with c~ = cy - p and n = Xo - cx:
+//   d2 = n^2 + (cy - y)^2 = n^2 + c~^2 - 4 h c~ + 4 h^2,  so  D = d2 - 4 h^2 = Q - 4 h c~, Q = n^2 + c~^2.
+// 4 h^2 is common to the nine candidates of the pixel.  Squares are 0 or 1 mod 4, so with
+//   Qh = (n^2 >> 2) + (c~^2 >> 2)  (< 2^31)  and  Ql = (n & 1) + (c~ & 1)  (in {0, 1, 2}):
+//   D >> 2 = Qh - h c~  (ONE integer multiply-add per candidate, in [-2^30, 2^31)),  D & 3 = Ql.
+// The key (d2, c) is then, for one pixel, the same order as (hi, lo) with hi = Qh - h c~ and
+//   lo = Ql 2^18 + cy 2 + [n < 0]
+// (equal d2 and equal cy leave |dx| equal: the two labels are mirror images about the pixel's
+// column, and the one with dx < 0, the smaller cx, wins).  The nine-way minimum is the walk_sk
+// "resolve later" pair: m = min hi (signed), then min over max(m - hi, lo) (unsigned): for hi > m
+// the difference wraps to >= 2^31 (hi - m <= 2 65535^2 / 4 + 1 < 2^31), above every lo (< 2^20).
+// The label is decoded from the winner: cy and the sign from lo, |dx| = sqrt(d2 - dy^2) with
+// d2 = 4 m + Ql + 4 h^2 (exact in uint32 arithmetic: dx^2 < 2^32; the float square root of a perfect
+// square below 2^32 rounds to the exact root).
+// Per staged label (once per row, shared by its up to three column uses, k a multiple of 4):
+//   Qh(n +- k) = Qh(n) + k^2/4 +- (k/2) n,  lo(n +- k) = lo(n) - [n < 0] + [n +- k < 0].
+// EMPTY (MAY_EMPTY): hi = INT_MAX (c~ = 0, Qh = INT_MAX), above every real hi (<= 2147418112); an
+// output whose minimum is INT_MAX stays EMPTY.
+struct RowW {
+  int32_t cyt[6];                 // c~ = cy - p of slot s (0 for EMPTY)
+  uint32_t qL[4], qC[4], qR[4];   // Qh of output e's left / centre / right candidate (slots e, e+1, e+2)
+  uint32_t lL[4], lC[4], lR[4];   // lo of the same
+};
+
+__device__ __forceinline__ uint32_t isqrt_square(uint32_t v) {  // v = a^2 < 2^32 -> a
+  const float f = __uint2float_rn(v);
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(f));
+  return __float2uint_rn(r);
+}
+
+// Terms of one staged row.  lab[s]: label of slot s (column X + (s-1) k); Xo: the thread's output
+// columns.  Slots 1..4 sit on output columns (their n is exact); slots 0 and 5 serve one output each
+// (output 0's left, output 3's right) and are computed against that output's column directly.
+#ifndef VD_WSK_SGN
+#define VD_WSK_SGN 1  // sign bits of lo: 1 = high word of 2n on the FMA pipe (IMAD.HI), 0 = shift + or (ALU)
+#endif
+__device__ __forceinline__ uint32_t add_sign(uint32_t lob, int n) {  // lob + [n < 0]
+#if VD_WSK_SGN
+  return mad_hi_u32((uint32_t)n, 2u, lob);
+#else
+  return lob + ((uint32_t)n >> 31);
+#endif
+}
+template <bool MAY_EMPTY>
+__device__ __forceinline__ void build_w(const uint32_t (&lab)[6], const int (&Xo)[4], uint32_t p, uint32_t k,
+                                        uint32_t k2q, uint32_t kh, RowW& R) {
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const uint32_t c = lab[s];
+    const uint32_t cy = c >> 16, cx = c & 0xFFFFu;
+    const int cyt = (int)(cy - p);
+    const uint32_t cy2 = (uint32_t)(cyt * cyt);
+    const int col = s == 0 ? Xo[0] : s == 5 ? Xo[3] : Xo[s - 1];
+    const int n = col - (int)cx;
+    const uint32_t n2 = (uint32_t)(n * n);
+    const uint32_t qh = (n2 >> 2) + (cy2 >> 2);
+    // Ql = (n^2 + c~^2) mod 4 (the square sum mod 2^32 keeps its low bits); lo base (Ql, cy, 0)
+    const uint32_t lob = (((n2 + cy2) << 18) & (3u << 18)) + 2u * cy;
+    const bool E = MAY_EMPTY && c == EMPTY;
+    constexpr uint32_t BIG = 0x7FFFFFFFu;
+    if (s == 0) {
+      R.qL[0] = E ? BIG : qh;
+      R.lL[0] = add_sign(lob, n);
+    } else if (s == 5) {
+      R.qR[3] = E ? BIG : qh;
+      R.lR[3] = add_sign(lob, n);
+    } else {
+      R.qC[s - 1] = E ? BIG : qh;
+      R.lC[s - 1] = add_sign(lob, n);
+      const uint32_t t = qh + k2q;
+      if (s <= 3) {  // left candidate of output s: column Xo + k
+        R.qL[s] = E ? BIG : t + kh * (uint32_t)n;
+        R.lL[s] = add_sign(lob, n + (int)k);
+      }
+      if (s >= 2) {  // right candidate of output s - 2: column Xo - k
+        R.qR[s - 2] = E ? BIG : t - kh * (uint32_t)n;
+        R.lR[s - 2] = add_sign(lob, n - (int)k);
+      }
+    }
+    R.cyt[s] = E ? 0 : cyt;
+  }
+}
+
+// Output label of column Xo[e] in row y (h = y >> 1, hh = 4 h^2) from the rows above (A), at (B),
+// below (Cn).  Returns EMPTY when every candidate is EMPTY.
+template <bool MAY_EMPTY>
+__device__ __forceinline__ uint32_t best_w(const RowW& A, const RowW& B, const RowW& Cn, int e, int Xo, int y,
+                                           uint32_t mh, uint32_t hh) {
+  int hi[9];
+  uint32_t lo[9];
+  auto put = [&](const RowW& R, int j) {
+    hi[3 * j + 0] = (int)(R.qL[e] + (uint32_t)R.cyt[e] * mh);
+    hi[3 * j + 1] = (int)(R.qC[e] + (uint32_t)R.cyt[e + 1] * mh);
+    hi[3 * j + 2] = (int)(R.qR[e] + (uint32_t)R.cyt[e + 2] * mh);
+    lo[3 * j + 0] = R.lL[e];
+    lo[3 * j + 1] = R.lC[e];
+    lo[3 * j + 2] = R.lR[e];
+  };
+  put(A, 0);
+  put(B, 1);
+  put(Cn, 2);
+  const int m = __vimin3_s32(__vimin3_s32(hi[0], hi[1], hi[2]), __vimin3_s32(hi[3], hi[4], hi[5]),
+                             __vimin3_s32(hi[6], hi[7], hi[8]));
+  uint32_t w[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) w[i] = __viaddmax_u32((uint32_t)m, 0u - (uint32_t)hi[i], lo[i]);
+  const uint32_t ww = __vimin3_u32(__vimin3_u32(w[0], w[1], w[2]), __vimin3_u32(w[3], w[4], w[5]),
+                                   __vimin3_u32(w[6], w[7], w[8]));
+  const uint32_t cy = (ww >> 1) & 0xFFFFu;
+  const int dy = (int)cy - y;
+  const uint32_t dx2 = (uint32_t)m * 4u + (ww >> 18) + hh - (uint32_t)(dy * dy);
+  const uint32_t ad = isqrt_square(dx2);
+  const uint32_t cx = (ww & 1u) ? (uint32_t)Xo + ad : (uint32_t)Xo - ad;
+  const uint32_t lab = (cy << 16) | cx;
+  if (MAY_EMPTY && m == 0x7FFFFFFF) return EMPTY;
+  return lab;
+}
+
+template <bool MAY_EMPTY, bool BANDED, bool FIX, bool FULL>
+__device__ __forceinline__ void walk_wsk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
+                                         uint32_t* smem) {
+  const int k = a.k;
+  const int tid = (int)threadIdx.x;
+  const int nw = FULL ? min(a.nwalk, k - (y0 - a.y_lo)) : 1;
+  const int nout = FULL ? (a.y_hi - y0 + k - 1) >> a.lk : min(a.walk, (a.y_hi - y0 + k - 1) >> a.lk);
+  const int nlist = FULL ? nw * nout : nout + 2;
+  const int SE = stage_elems_sk(k);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(a.walk + 2) * SE);
+  stage_walk<FULL, BANDED>(a, tm, x0, y0, k, nout, nlist, true, (k + 3) & ~3, SE, smem, bars);
+
+  int Xo[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) Xo[e] = X + e * k;
+  const bool left_out = FIX && X - k < 0;
+  const int nc = FIX ? (X >= a.N ? 0 : ((a.N - 1 - X) >> a.lk) + 1) : 8;  // in-grid slot columns (walk_sk)
+  const uint32_t uk = (uint32_t)k, k2q = uk * uk / 4u, kh = uk / 2u;
+  bool any_empty = false;
+
+  auto consume = [&](int i, uint32_t p, RowW& R) {
+    mbar_wait(&bars[i], 0u);
+    const uint32_t* st = smem + (size_t)i * SE + tid;
+    uint32_t lab[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) lab[s] = st[s * 128];
+    if constexpr (FIX) {  // an out-of-grid neighbour column -> the same output's centre label (a duplicate)
+      lab[0] = left_out ? lab[1] : lab[0];
+#pragma unroll
+      for (int s = 1; s < 6; ++s) lab[s] = s >= nc + 1 ? lab[s - 1] : lab[s];
+    }
+    build_w<MAY_EMPTY>(lab, Xo, p, uk, k2q, kh, R);
+  };
+
+  const int64_t kp = (int64_t)k * a.pitch;
+  auto run = [&](int yw, int n, int ibase) {
+    const uint32_t p = (uint32_t)yw & 1u;
+    RowW r0, r1, r2;
+    if constexpr (FULL) {
+      consume(ibase + 1, p, r1);
+      r0 = r1;
+    } else {
+      consume(ibase, p, r0);
+      consume(ibase + 1, p, r1);
+    }
+    int y = yw;
+    uint32_t* po = a.out + (int64_t)(yw - a.row0) * a.pitch + X;
+    int j = 0;
+    auto step = [&](const RowW& Pv, const RowW& Cv, RowW& Nx) -> bool {
+      if (!FULL || j + 1 < n) consume(ibase + j + 2, p, Nx);
+      else Nx = Cv;
+      const uint32_t h = (uint32_t)y >> 1;
+      const uint32_t mh = 0u - h, hh = 4u * h * h;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t o = best_w<MAY_EMPTY>(Pv, Cv, Nx, e, Xo[e], y, mh, hh);
+        if (e < nc) {
+          if (MAY_EMPTY) any_empty |= o == EMPTY;
+          store_out(a, BANDED, y, Xo[e], po + e * k, o);
+        }
+      }
+      po += kp;
+      y += k;
+      return ++j < n;
+    };
+#pragma unroll 1
+    while (true) {
+      if (!step(r0, r1, r2)) break;
+      if (!step(r1, r2, r0)) break;
+      if (!step(r2, r0, r1)) break;
+    }
+  };
+  if constexpr (FULL) {
+#pragma unroll 1
+    for (int w = 0; w < nw; ++w) run(y0 + w, nout, w * nout - 1);
+  } else {
+    run(y0, nout, 0);
+  }
+  if (a.loc_out && tid == 0) atomicOr(a.loc_out, 1u);  // locality is not tracked on this path
+  if (MAY_EMPTY && a.empty_flag != nullptr && __syncthreads_or(any_empty) && tid == 0) atomicOr(a.empty_flag, 1ull);
+}
+
+// grid as jump_pass_sk with k >= 256 (groups of 4k columns, k / 128 residue blocks each); runtime k.
+template <bool MAY_EMPTY, bool BANDED>
+__global__ void __launch_bounds__(kThreads, VD_MIN_BLOCKS) jump_pass_wsk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(128) uint32_t dyn_smem[];
+  const int xb = (int)blockIdx.x;
+  const bool full = a.nwalk > 0;
+  const int seg = full ? 0 : (int)(a.res_in_y ? blockIdx.z : blockIdx.y);
+  const int res = full ? (int)blockIdx.z * a.nwalk : (int)(a.res_in_y ? blockIdx.y : blockIdx.z);
+  const int y0 = a.y_lo + res + seg * a.walk * a.k;
+  if (res >= a.k || y0 >= a.y_hi) return;  // (uniform: the whole CTA leaves)
+  const int k = a.k;
+  const int lr = a.lk - 7;  // k / 128 residue blocks per group of 4k columns
+  const int g = xb >> lr, rb = xb & ((1 << lr) - 1);
+  const int x0 = 4 * k * g + 128 * rb;
+  if (x0 >= a.N) return;  // (the partial last group of a grid that is not a multiple of 4k)
+  const int X = x0 + (int)threadIdx.x;
+  const bool fix = g == 0 || x0 + 4 * k + 128 > a.N;  // some right neighbour column (X + 4k) beyond the grid
+  if (full) {
+    if (fix) walk_wsk<MAY_EMPTY, BANDED, true, true>(a, &tm, x0, X, y0, dyn_smem);
+    else walk_wsk<MAY_EMPTY, BANDED, false, true>(a, &tm, x0, X, y0, dyn_smem);
+  } else {
+    if (fix) walk_wsk<MAY_EMPTY, BANDED, true, false>(a, &tm, x0, X, y0, dyn_smem);
+    else walk_wsk<MAY_EMPTY, BANDED, false, false>(a, &tm, x0, X, y0, dyn_smem);
+  }
 }
 
 // ------------------------------------------------------------------ wide jump pass
@@ -1409,9 +1682,9 @@ __global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __r
 // new = clamp(old + disp) per axis (R-10; the reserved pixel at N = 65536, R-4), then
 // fwd[old] <- min(fwd[old], new): co-located seeds leave the smallest new label.  fwd is
 // all EMPTY between dJFA steps (reset_stamp restores it).
-// flag_g (or null): the fused frame (NEXT-1) also re-stamps the new seed pixel here, BEFORE the
-// first pass, with bit 31 set so that the pass's in-stage remap leaves it as it is (R-9: remap,
-// then re-stamp).  Labels are < 2^31 for N <= 32768, so the flag is free.  One band, rows [0, N).
+// flag_g (or null): the fused frame (NEXT-1) also marks the new seed pixel here, BEFORE the first
+// pass, with EMPTY, which the pass's in-stage remap turns into the pixel's own position (R-9:
+// remap, then re-stamp).  A dJFA diagram holds no EMPTY, so the marker is free.  One band.
 __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __restrict__ disp,
                          uint32_t* __restrict__ new_s, uint32_t* __restrict__ fwd, int64_t s, int N,
                          uint32_t* __restrict__ flag_g = nullptr, int64_t pitch = 0) {
@@ -1425,7 +1698,7 @@ __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __res
     const uint32_t nw = ((uint32_t)y << 16) | (uint32_t)x;
     new_s[i] = nw;
     atomicMin(&fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)], nw);
-    if (flag_g) flag_g[(int64_t)y * pitch + x] = nw | 0x80000000u;
+    if (flag_g) flag_g[(int64_t)y * pitch + x] = EMPTY;  // marker: "new seed here" (jump_pass_sk_remap)
   }
 }
 

@@ -40,6 +40,10 @@ inline cudaError_t launch_sk(int dev, uint32_t k, bool me, bool bd, bool five, b
 cudaError_t launch_sk_remap(int dev, uint32_t k, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk,
                             size_t smem, cudaStream_t st);
 
+// jump_pass_wsk (wide exact pass for N <= 65536, EMPTY allowed): power-of-two 256 <= k <= N / 4.
+cudaError_t launch_wsk(int dev, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm, dim3 grid, dim3 blk,
+                       size_t smem, cudaStream_t st);
+
 // jump_pass_wide (generic 64-bit pass: any k, any N <= 65536, EMPTY allowed).
 cudaError_t launch_wide(uint32_t k, int metric, bool vn, const vdk::PassArgs& a, dim3 grid, dim3 blk,
                         cudaStream_t st);

@@ -46,6 +46,24 @@ def test_jfa_bit_exact(vd, N, s):
     assert d.last_passes() == len(oracle.jfa_schedule(N))
 
 
+# Multiples of 512 that 4k does not divide for some k >= 256: the shared-term kernel's last group
+# of 4k columns is partial (outputs beyond the grid not stored, slots beyond it duplicated), and
+# where k does not divide N the rows are staged span by span instead of by one tensor copy.
+@pytest.mark.parametrize("N,s", [(1536, 300), (2560, 700), (3584, 1000), (6656, 5000)])
+def test_jfa_partial_span_groups_bit_exact(vd, N, s):
+    xy = synth.uniform_seeds(N, s, rng_seed=N + 7)
+    d = _jfa_gpu(vd, N, xy)
+    assert np.array_equal(d.labels(), oracle.jfa(N, xy))
+    rng = np.random.default_rng(N)
+    G = ((rng.integers(0, N, (N, N)) << 16) | rng.integers(0, N, (N, N))).astype(np.uint32)
+    for k in (256, 512, 1024):
+        if 4 * k <= N:
+            d.set_labels(G)
+            d.jump_pass(k)
+            assert np.array_equal(d.labels(), oracle.jump_pass(G, k)), k
+    d.close()
+
+
 @pytest.mark.parametrize("extras", [1, 2])
 def test_jfa_extras_bit_exact(vd, extras):
     N, s = 200, 60
@@ -478,6 +496,28 @@ def test_djfa_beyond_32768_sparse_seeds_bit_exact(vd):
     G, xy, n = oracle.djfa_step(N, xy, disp, dmax, G, inplace=True)
     assert d.last_passes() == n and d.last_packed_passes() == 0
     assert np.array_equal(d.labels(), G)
+    d.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("s,packed", [(1 << 22, False), (1 << 23, True)])
+def test_djfa_fused_remap_beyond_32768_bit_exact(vd, s, packed):
+    # dJFA frames beyond N = 32768 with the remap fused into the first pass (the new seed pixels
+    # marked EMPTY by move_fwd, labels 32 bits wide): delta_1 = 64 takes the fused pass's exact
+    # 64-bit walk (X64), delta_1 = 32 its packed walk.  Every pixel against the oracle.
+    N, dmax = 33280, 1
+    xy = synth.uniform_seeds(N, s, rng_seed=s)
+    d = _jfa_gpu(vd, N, xy)
+    G = oracle.jfa(N, xy)
+    assert np.array_equal(d.labels(), G)
+    for f in range(2):
+        disp = synth.displacements(s, dmax, f, rng_seed=s)
+        d.djfa_step(disp, dmax)
+        G, xy, n = oracle.djfa_step(N, xy, disp, dmax, G, inplace=True)
+        assert d.last_passes() == n
+        if packed and f == 1:  # (frame 0 follows JFA, whose last passes may not report locality)
+            assert d.last_packed_passes() == n
+        assert np.array_equal(d.labels(), G), f
     d.close()
 
 
