@@ -942,6 +942,10 @@ __device__ __forceinline__ void stage_walk(const PassArgs& a, const CUtensorMap*
 // HASH (the last pass of an e2e dJFA step, KM = 1): every output label is also added to the
 // frame's checksum, sum over p of fmix32((y N + x) * 0x9E3779B9 ^ label) mod 2^64 (label_hash),
 // so the step needs no separate 4-B/px read for its result.
+#ifndef VD_FUSE_LA
+#define VD_FUSE_LA 1  // rows of fwd-gather look-ahead in the fused remap pass (1 or 2)
+#endif
+constexpr int kFuseLA = VD_FUSE_LA;
 template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false,
           bool X64 = false, bool HASH = false>
 __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
@@ -1042,8 +1046,11 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
 #pragma unroll
       for (int s = 0; s < KS; ++s) lab[s] = left_out ? lab[s + KS] : lab[s];
       if constexpr (STRIDE) {
+        if (nc < 4) {  // the partial last group of 4k columns (spans on a grid that 4k does not divide)
 #pragma unroll
-        for (int s = 1; s < NS; ++s) lab[s] = s >= nc + 1 ? lab[s - 1] : lab[s];
+          for (int s = 1; s < NS - 1; ++s) lab[s] = s >= nc + 1 ? lab[s - 1] : lab[s];
+        }
+        lab[NS - 1] = right_out ? lab[NS - 2] : lab[NS - 1];
       } else {
 #pragma unroll
         for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
@@ -1058,7 +1065,8 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   // rows 0 and n + 1 in the stage (outside the grid: the centre row is a duplicate candidate).
   auto run = [&](int yw, int n, int ibase) {
     R_t r0, r1, r2;
-    uint32_t pend[NS];  // REMAP: the next row's remapped slot labels
+    uint32_t pend[NS];   // REMAP: the next row's remapped slot labels
+    uint32_t pend2[NS];  // ... and, with two rows of look-ahead (VD_FUSE_LA = 2), the row after
     if constexpr (REMAP) {
       uint32_t l0[NS];
       fetch(ibase, l0);
@@ -1066,9 +1074,9 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       build_sk<KS, MAY_EMPTY, PACK>(l0, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, r0);
       build_sk<KS, MAY_EMPTY, PACK>(pend, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, r1);
       fetch(ibase + 2, pend);
+      if (kFuseLA == 2 && 3 < n + 2) fetch(ibase + 3, pend2);
     } else if constexpr (FULL) {
-      consume(ibase + 1, r1);
-      r0 = r1;
+      consume(ibase + 1, r1);  // (the row above the first output is outside the grid: r1 serves as both)
     } else {
       consume(ibase, r0);
       consume(ibase + 1, r1);
@@ -1076,22 +1084,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
     int y = yw;
     uint32_t* po = a.out + (int64_t)(yw - a.row0) * a.pitch + X;
     int j = 0;
-    auto step = [&](const R_t& Pv, const R_t& Cv, R_t& Nx) -> bool {
-      if constexpr (REMAP) {
-        build_sk<KS, MAY_EMPTY, PACK>(pend, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, Nx);
-        if (j + 3 < n + 2) fetch(ibase + j + 3, pend);  // gathers in flight during this row
-        if (a.prefetch && j + 4 < n + 2) {  // and the row after that: its fwd lines into L1
-          mbar_wait(&bars[ibase + j + 4], 0u);
-          const uint32_t* st = smem + (size_t)(ibase + j + 4) * SE;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            const uint32_t c = st[sbase + s * (spans ? 128 : k)];
-            if (c != EMPTY)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu))));
-          }
-        }
-      } else if (!FULL || j + 1 < n) consume(ibase + j + 2, Nx);
-      else Nx = Cv;
+    auto eval = [&](const R_t& Pv, const R_t& Cv, const R_t& Nx) {
       uint32_t o[kVec];
       if constexpr (X64) {
 #pragma unroll
@@ -1139,13 +1132,52 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       }
       po += kp;
       y += k;
+    };
+    auto step = [&](const R_t& Pv, const R_t& Cv, R_t& Nx) -> bool {
+      if constexpr (REMAP) {
+        build_sk<KS, MAY_EMPTY, PACK>(pend, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, Nx);
+        if constexpr (kFuseLA == 2) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s) pend[s] = pend2[s];
+          if (j + 4 < n + 2) fetch(ibase + j + 4, pend2);  // gathers in flight during two rows
+        } else {
+          if (j + 3 < n + 2) fetch(ibase + j + 3, pend);  // gathers in flight during this row
+        }
+        if (a.prefetch && j + 3 + kFuseLA < n + 2) {  // and the row after that: its fwd lines into L1
+          mbar_wait(&bars[ibase + j + 3 + kFuseLA], 0u);
+          const uint32_t* st = smem + (size_t)(ibase + j + 3 + kFuseLA) * SE;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const uint32_t c = st[sbase + s * (spans ? 128 : k)];
+            if (c != EMPTY)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu))));
+          }
+        }
+        eval(Pv, Cv, Nx);
+      } else if (!FULL || j + 1 < n) {
+        consume(ibase + j + 2, Nx);
+        eval(Pv, Cv, Nx);
+      } else {
+        eval(Pv, Cv, Cv);  // FULL: the row below the last output is outside the grid
+      }
       return ++j < n;
     };
+    if (FULL) {
+      if (step(r1, r1, r2)) {
 #pragma unroll 1
-    while (true) {
-      if (!step(r0, r1, r2)) break;
-      if (!step(r1, r2, r0)) break;
-      if (!step(r2, r0, r1)) break;
+        while (true) {
+          if (!step(r1, r2, r0)) break;
+          if (!step(r2, r0, r1)) break;
+          if (!step(r0, r1, r2)) break;
+        }
+      }
+    } else {
+#pragma unroll 1
+      while (true) {
+        if (!step(r0, r1, r2)) break;
+        if (!step(r1, r2, r0)) break;
+        if (!step(r2, r0, r1)) break;
+      }
     }
   };
   if constexpr (FULL) {
@@ -1305,17 +1337,19 @@ __device__ __forceinline__ uint32_t add_sign(uint32_t lob, int n) {  // lob + [n
   return lob + ((uint32_t)n >> 31);
 #endif
 }
+// (one = 1 and sh16 = 2^16 are run-time values, so that the additions below stay IMADs on the FMA
+// pipe: the pass is ALU-bound)
 template <bool MAY_EMPTY>
 __device__ __forceinline__ void build_w(const uint32_t (&lab)[6], const int (&Xo)[4], uint32_t p, uint32_t k,
-                                        uint32_t k2q, uint32_t kh, RowW& R) {
+                                        uint32_t k2q, uint32_t kh, uint32_t one, uint32_t sh16, RowW& R) {
 #pragma unroll
   for (int s = 0; s < 6; ++s) {
     const uint32_t c = lab[s];
-    const uint32_t cy = c >> 16, cx = c & 0xFFFFu;
-    const int cyt = (int)(cy - p);
+    const uint32_t cy = c >> 16;
+    const int cyt = (int)(cy * one - p);
     const uint32_t cy2 = (uint32_t)(cyt * cyt);
     const int col = s == 0 ? Xo[0] : s == 5 ? Xo[3] : Xo[s - 1];
-    const int n = col - (int)cx;
+    const int n = (int)(cy * sh16 + ((uint32_t)col - c));  // col - cx, with cx = c - cy 2^16
     const uint32_t n2 = (uint32_t)(n * n);
     const uint32_t qh = (n2 >> 2) + (cy2 >> 2);
     // Ql = (n^2 + c~^2) mod 4 (the square sum mod 2^32 keeps its low bits); lo base (Ql, cy, 0)
@@ -1334,11 +1368,11 @@ __device__ __forceinline__ void build_w(const uint32_t (&lab)[6], const int (&Xo
       const uint32_t t = qh + k2q;
       if (s <= 3) {  // left candidate of output s: column Xo + k
         R.qL[s] = E ? BIG : t + kh * (uint32_t)n;
-        R.lL[s] = add_sign(lob, n + (int)k);
+        R.lL[s] = add_sign(lob, (int)((uint32_t)n * one + k));
       }
       if (s >= 2) {  // right candidate of output s - 2: column Xo - k
         R.qR[s - 2] = E ? BIG : t - kh * (uint32_t)n;
-        R.lR[s - 2] = add_sign(lob, n - (int)k);
+        R.lR[s - 2] = add_sign(lob, (int)((uint32_t)n * one - k));
       }
     }
     R.cyt[s] = E ? 0 : cyt;
@@ -1408,10 +1442,13 @@ __device__ __forceinline__ void walk_wsk(const PassArgs& a, const CUtensorMap* t
     for (int s = 0; s < 6; ++s) lab[s] = st[s * 128];
     if constexpr (FIX) {  // an out-of-grid neighbour column -> the same output's centre label (a duplicate)
       lab[0] = left_out ? lab[1] : lab[0];
+      if (nc < 4) {  // the partial last group of 4k columns
 #pragma unroll
-      for (int s = 1; s < 6; ++s) lab[s] = s >= nc + 1 ? lab[s - 1] : lab[s];
+        for (int s = 1; s < 5; ++s) lab[s] = s >= nc + 1 ? lab[s - 1] : lab[s];
+      }
+      lab[5] = nc <= 4 ? lab[4] : lab[5];
     }
-    build_w<MAY_EMPTY>(lab, Xo, p, uk, k2q, kh, R);
+    build_w<MAY_EMPTY>(lab, Xo, p, uk, k2q, kh, a.one, a.sh16, R);
   };
 
   const int64_t kp = (int64_t)k * a.pitch;
@@ -1419,8 +1456,7 @@ __device__ __forceinline__ void walk_wsk(const PassArgs& a, const CUtensorMap* t
     const uint32_t p = (uint32_t)yw & 1u;
     RowW r0, r1, r2;
     if constexpr (FULL) {
-      consume(ibase + 1, p, r1);
-      r0 = r1;
+      consume(ibase + 1, p, r1);  // (the row above the first output is outside the grid: r1 serves as both)
     } else {
       consume(ibase, p, r0);
       consume(ibase + 1, p, r1);
@@ -1428,9 +1464,7 @@ __device__ __forceinline__ void walk_wsk(const PassArgs& a, const CUtensorMap* t
     int y = yw;
     uint32_t* po = a.out + (int64_t)(yw - a.row0) * a.pitch + X;
     int j = 0;
-    auto step = [&](const RowW& Pv, const RowW& Cv, RowW& Nx) -> bool {
-      if (!FULL || j + 1 < n) consume(ibase + j + 2, p, Nx);
-      else Nx = Cv;
+    auto eval = [&](const RowW& Pv, const RowW& Cv, const RowW& Nx) {
       const uint32_t h = (uint32_t)y >> 1;
       const uint32_t mh = 0u - h, hh = 4u * h * h;
 #pragma unroll
@@ -1443,13 +1477,32 @@ __device__ __forceinline__ void walk_wsk(const PassArgs& a, const CUtensorMap* t
       }
       po += kp;
       y += k;
+    };
+    auto step = [&](const RowW& Pv, const RowW& Cv, RowW& Nx) -> bool {
+      if (!FULL || j + 1 < n) {
+        consume(ibase + j + 2, p, Nx);
+        eval(Pv, Cv, Nx);
+      } else {
+        eval(Pv, Cv, Cv);  // FULL: the row below the last output is outside the grid
+      }
       return ++j < n;
     };
+    if (FULL) {
+      if (step(r1, r1, r2)) {
 #pragma unroll 1
-    while (true) {
-      if (!step(r0, r1, r2)) break;
-      if (!step(r1, r2, r0)) break;
-      if (!step(r2, r0, r1)) break;
+        while (true) {
+          if (!step(r1, r2, r0)) break;
+          if (!step(r2, r0, r1)) break;
+          if (!step(r0, r1, r2)) break;
+        }
+      }
+    } else {
+#pragma unroll 1
+      while (true) {
+        if (!step(r0, r1, r2)) break;
+        if (!step(r1, r2, r0)) break;
+        if (!step(r2, r0, r1)) break;
+      }
     }
   };
   if constexpr (FULL) {
