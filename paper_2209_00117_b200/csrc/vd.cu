@@ -151,6 +151,7 @@ struct vd_ctx {
   int metric = 0;           // 0 Euclidean (dJFAe), 1 Manhattan (dJFAm)
   uint32_t vn_waves = 0;    // Von Neumann waves at the start of each dJFA step
   bool force_rel = false;   // test hook (env VD_FORCE_WINDOWED=1): windowed kernel at any N
+  bool force_wsk = false;   // test hook (env VD_FORCE_WSK=1): the wide exact pass at any N (its arithmetic holds for N <= 65536)
   bool track_empty = false; // jump_pass_wide reports EMPTY outputs into `counter` (vd_jfa)
   uint32_t jfa_vn_waves = 0;// ... and of each full JFA (Fig. 5)
   uint32_t hcap = 0;  // halo rows allocated per side
@@ -421,6 +422,7 @@ bool sk_ok(const vd_ctx* h, uint32_t k, bool vn, bool may_empty) {
   // beyond 32768 only inside dJFA frames, whose inputs are local (packed walk); JFA's passes there
   // are never local and keep the windowed exact walk, which beats 64-bit keys
   if (h->force_rel || (h->N > 32768 && (may_empty || k > (uint32_t)vdk::kPackMaxK || !h->in_djfa))) return false;
+  if (h->force_wsk && k >= 256) return false;  // (test hook: those steps go to the wide pass)
   if (may_empty && h->N > 16384) return false;  // the virtual far seed needs 2N - 1 < 2^15 (as jump_pass_fast)
   return !off && ((mask >> lk) & 1) && !vn && h->metric == 0 && h->N % 512 == 0 && 4 * k <= h->N;
 }
@@ -456,7 +458,7 @@ bool encode_span_map(const vd_ctx* h, const uint32_t* in, uint32_t rows, uint32_
 // at C5).  VD_NO_WSK=1 disables it (A/B against the windowed / 64-bit kernels).
 bool wsk_ok(const vd_ctx* h, uint32_t k, bool vn) {
   static const bool off = [] { const char* e = getenv("VD_NO_WSK"); return e && e[0] == '1'; }();
-  return !off && !h->force_rel && h->N > 32768 && h->N % 512 == 0 && h->metric == 0 && !vn && k >= 256 &&
+  return !off && !h->force_rel && (h->N > 32768 || h->force_wsk) && h->N % 512 == 0 && h->metric == 0 && !vn && k >= 256 &&
          (k & (k - 1)) == 0 && 4 * k <= h->N;
 }
 
@@ -545,7 +547,7 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     // the fused remap pass defaults to segment-slowest order: concurrent CTAs then cover a band
     // of rows, whose seeds' fwd entries stay in L2 (VD_FUSE_ORDER=0: residue slowest)
     static const int fuse_order = [] { const char* e = getenv("VD_FUSE_ORDER"); return e ? atoi(e) : 1; }();
-    a.res_in_y = (h->fuse_remap ? fuse_order : order) == 1 ? 1 : 0;
+    a.res_in_y = h->fuse_remap ? (fuse_order == 1 || fuse_order == 2 ? fuse_order : 0) : (order == 1 ? 1 : 0);
     // Whole residue classes per CTA (jump_pass_sk FULL walks) when one class fits the stage: a
     // one-band pass over the whole grid with k >= N / (walk + 2) (JFA's large steps).
     // VD_NO_FULL=1 disables it (A/B).
@@ -554,12 +556,15 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
     a.nwalk = 0;
     unsigned gz = a.res_in_y ? (unsigned)a.segs : nres, gy = a.res_in_y ? nres : (unsigned)a.segs;
     if ((sk || wsk) && !h->fuse_remap && !no_full && !banded && y_lo == 0 && y_hi == (int64_t)h->N && h->N % k == 0) {
-      const uint32_t per = h->N / k, fit = (uint32_t)vdk::walk_len_sk((int)k) + 2;
-      if (4 * per <= fit) {  // (one or two classes per CTA measured slower than segment walks)
+      const uint32_t per = h->N / k, fit = (uint32_t)vdk::walk_len_sk((int)k, budget) + 2;  // (the launch's stage budget)
+      // (at least two classes per CTA: C4's k = 2048 0.555 -> 0.522 ms against segment walks, once the
+      // FULL walks stopped copying rows; one class per CTA is slower.  VD_FULL_MIN=m: at least m, A/B)
+      static const uint32_t full_min = [] { const char* e = getenv("VD_FULL_MIN"); return e ? (uint32_t)atoi(e) : 2u; }();
+      if (full_min * per <= fit) {
         // as many classes per CTA as fit, but keep >= 4 CTAs per SM in the grid
         const int64_t cap = std::max<int64_t>(1, (int64_t)a.xblocks * k / ((int64_t)h->num_sms * 4));
         a.nwalk = (int)std::min<int64_t>(fit / per, cap);
-        a.walk = vdk::walk_len_sk((int)k);
+        a.walk = vdk::walk_len_sk((int)k, budget);
         a.segs = 1;
         a.res_in_y = 0;
         gy = 1;
@@ -600,7 +605,9 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
         a.prefetch = pf;
         a.loc_in = h->pass_loc_in;  // the previous frame's locality, when the moves keep the packed key valid
         a.nwalk = 0;
-        const dim3 g2((unsigned)a.xblocks, a.res_in_y ? nres : (unsigned)a.segs, a.res_in_y ? (unsigned)a.segs : nres);
+        const dim3 g2 = a.res_in_y == 2 ? dim3(nres, (unsigned)a.xblocks, (unsigned)a.segs)
+                                        : dim3((unsigned)a.xblocks, a.res_in_y ? nres : (unsigned)a.segs,
+                                               a.res_in_y ? (unsigned)a.segs : nres);
         e = vdl::launch_sk_remap(h->device, k, a, tm, g2, blk, sm, h->stream);
       } else {
         if (k == 1 && h->hash_pass && !may_empty) a.hash_out = h->counter;  // the frame's last pass also sums the checksum
@@ -981,6 +988,8 @@ vd_status vd_create(vd_handle* out, uint32_t N, uint64_t s, const uint16_t* seed
   {
     const char* f = std::getenv("VD_FORCE_WINDOWED");
     h->force_rel = f && f[0] == '1';
+    const char* w = std::getenv("VD_FORCE_WSK");
+    h->force_wsk = w && w[0] == '1';
   }
   h->vn_waves = cfg.vn_waves;
   h->jfa_vn_waves = cfg.jfa_vn_waves;
@@ -1205,9 +1214,10 @@ vd_status enqueue_label_hash(vd_ctx* h);
 // accumulated by the last pass when it can (jump_pass_sk HASH, k = 1), else by label_hash.
 vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash) {
   NvtxRange range("vd_djfa_step");
-  if (!h->fwd) {  // forward map, kept all-EMPTY between steps
-    CK(cudaMalloc(&h->fwd, (size_t)h->N * h->N * sizeof(uint32_t)));
-    CK(cudaMemsetAsync(h->fwd, 0xFF, (size_t)h->N * h->N * sizeof(uint32_t), h->stream));
+  if (!h->fwd) {  // forward map, kept all-EMPTY between steps; indexed by the label itself ((y << 16) | x)
+    const size_t bytes = (size_t)h->N * 65536 * sizeof(uint32_t);
+    CK(cudaMalloc(&h->fwd, bytes));
+    CK(cudaMemsetAsync(h->fwd, 0xFF, bytes, h->stream));
   }
   std::vector<uint32_t> ks;
   schedule_djfa(h->N, h->s, d_max, h->extras, ks);

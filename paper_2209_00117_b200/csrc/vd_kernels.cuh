@@ -44,7 +44,8 @@ struct PassArgs {
   int32_t segs;     // walk segments per residue class: ceil(ceil(rows / k) / walk)
   int32_t walk;     // output rows per walk (walk_len(k))
   int32_t xblocks;  // CTAs across one row: ceil(N / (4 * kThreads))
-  int32_t res_in_y; // grid order: 0 = (x-block, segment, residue), 1 = (x-block, residue, segment)
+  int32_t res_in_y; // grid order: 0 = (x-block, segment, residue), 1 = (x-block, residue, segment),
+                    // 2 = (residue, x-block, segment) (jump_pass_sk_remap only)
   int32_t nwalk;    // jump_pass_sk: > 0 = whole residue classes, nwalk of them per CTA (FULL walks)
   int32_t tmap;     // jump_pass_sk, k >= 256, one band: stage each row's six spans with ONE tensor copy
   const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label)
@@ -942,6 +943,19 @@ __device__ __forceinline__ void stage_walk(const PassArgs& a, const CUtensorMap*
 // HASH (the last pass of an e2e dJFA step, KM = 1): every output label is also added to the
 // frame's checksum, sum over p of fmix32((y N + x) * 0x9E3779B9 ^ label) mod 2^64 (label_hash),
 // so the step needs no separate 4-B/px read for its result.
+#ifndef VD_FWD_HINT
+#define VD_FWD_HINT 0  // 1: the fused pass's fwd gathers carry an L2 evict_last policy (A/B)
+#endif
+__device__ __forceinline__ uint32_t ld_fwd(const uint32_t* p, uint64_t pol) {
+#if VD_FWD_HINT
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
 #ifndef VD_FUSE_LA
 #define VD_FUSE_LA 1  // rows of fwd-gather look-ahead in the fused remap pass (1 or 2)
 #endif
@@ -1000,6 +1014,10 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   uint64_t hacc = 0;  // HASH
   using R_t = RowS<NS>;
   // REMAP: slot labels of a staged row, remapped through fwd (loads in flight until build)
+  uint64_t fwd_pol = 0;
+#if VD_FWD_HINT
+  if constexpr (REMAP) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(fwd_pol));
+#endif
   auto fetch = [&](int i, uint32_t (&lab)[NS]) {
     if constexpr (!PRE) mbar_wait(&bars[i], 0u);
     const uint32_t* st = smem + (size_t)i * SE;
@@ -1024,7 +1042,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       uint32_t own = own0 + (uint32_t)(s * k);
       if (FIX && s == 0 && left_out) own += (uint32_t)k;
       if (FIX && s == NS - 1 && right_out) own -= (uint32_t)k;
-      lab[s] = c == EMPTY ? own : __ldg(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu)));
+      lab[s] = c == EMPTY ? own : ld_fwd(a.fwd + c, fwd_pol);  // (fwd is indexed by the label itself, pitch 2^16)
     }
   };
   auto consume = [&](int i, R_t& R) {
@@ -1150,7 +1168,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
           for (int s = 0; s < NS; ++s) {
             const uint32_t c = st[sbase + s * (spans ? 128 : k)];
             if (c != EMPTY)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fwd + ((c >> 16) * (uint32_t)N + (c & 0xFFFFu))));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fwd + c));
           }
         }
         eval(Pv, Cv, Nx);
@@ -1260,8 +1278,12 @@ __global__ void __launch_bounds__(kThreads, MINB) jump_pass_sk(PassArgs a, const
 template <int KM>
 __global__ void __launch_bounds__(kThreads, 5) jump_pass_sk_remap(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
-  const int xb = (int)blockIdx.x;
-  const int seg = (int)(a.res_in_y ? blockIdx.z : blockIdx.y), res = (int)(a.res_in_y ? blockIdx.y : blockIdx.z);
+  // grid order 2 = (residue, x-block, segment): the CTAs resident at once cover every residue class
+  // of a few 512-column blocks of one row band, so each fwd entry is gathered by all of them while
+  // it is in L2 (the other orders: see PassArgs::res_in_y)
+  const int xb = (int)(a.res_in_y == 2 ? blockIdx.y : blockIdx.x);
+  const int seg = (int)(a.res_in_y ? blockIdx.z : blockIdx.y);
+  const int res = (int)(a.res_in_y == 2 ? blockIdx.x : a.res_in_y ? blockIdx.y : blockIdx.z);
   const int y0 = a.y_lo + res + seg * a.walk * a.k;
   if (res >= a.k || y0 >= a.y_hi) return;
   const int tid = (int)threadIdx.x;
@@ -1411,6 +1433,16 @@ __device__ __forceinline__ uint32_t best_w(const RowW& A, const RowW& B, const R
   const uint32_t cx = (ww & 1u) ? (uint32_t)Xo + ad : (uint32_t)Xo - ad;
   const uint32_t lab = (cy << 16) | cx;
   if (MAY_EMPTY && m == 0x7FFFFFFF) return EMPTY;
+#ifdef VD_CHECK  // debug builds (compute-sanitizer is not available on the pool): the decoded label
+                 // must lie in the grid and reproduce the winning key exactly
+  {
+    const int64_t ddx = (int64_t)cx - Xo, ddy = (int64_t)cy - y;
+    const int64_t d2 = ddx * ddx + ddy * ddy;
+    if (cx > 65535u || d2 != 4 * (int64_t)m + (ww >> 18) + 4 * (int64_t)(y >> 1) * (y >> 1) ||
+        ((ww & 1u) != (cx > (uint32_t)Xo ? 1u : 0u) && ad != 0u))
+      __trap();
+  }
+#endif
   return lab;
 }
 
@@ -1733,7 +1765,8 @@ __global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __r
 
 // SimulateParticles (Alg. 1) fused with the forward map (R-9):
 // new = clamp(old + disp) per axis (R-10; the reserved pixel at N = 65536, R-4), then
-// fwd[old] <- min(fwd[old], new): co-located seeds leave the smallest new label.  fwd is
+// fwd[old] <- min(fwd[old], new): co-located seeds leave the smallest new label.  fwd is indexed
+// by the label value itself (rows of 2^16 entries, N rows: one address computation per lookup).  fwd is
 // all EMPTY between dJFA steps (reset_stamp restores it).
 // flag_g (or null): the fused frame (NEXT-1) also marks the new seed pixel here, BEFORE the first
 // pass, with EMPTY, which the pass's in-stage remap turns into the pixel's own position (R-9:
@@ -1750,7 +1783,7 @@ __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __res
     if (N == 65536 && x == 65535 && y == 65535) x = 65534;
     const uint32_t nw = ((uint32_t)y << 16) | (uint32_t)x;
     new_s[i] = nw;
-    atomicMin(&fwd[(int64_t)(c >> 16) * N + (c & 0xFFFFu)], nw);
+    atomicMin(&fwd[c], nw);
     if (flag_g) flag_g[(int64_t)y * pitch + x] = EMPTY;  // marker: "new seed here" (jump_pass_sk_remap)
   }
 }
@@ -1764,7 +1797,7 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     if (do_reset) {
       const uint32_t o = old_s[i];
-      fwd[(int64_t)(o >> 16) * N + (o & 0xFFFFu)] = EMPTY;
+      fwd[o] = EMPTY;
     }
     const uint32_t c = new_s[i];
     const int y = (int)(c >> 16) - row0, x = (int)(c & 0xFFFFu);
@@ -1777,7 +1810,7 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
 __global__ void fwd_reset(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s, int64_t s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = old_s[i];
-    fwd[(int64_t)(o >> 16) * N + (o & 0xFFFFu)] = EMPTY;
+    fwd[o] = EMPTY;
   }
 }
 
@@ -1809,7 +1842,7 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
       for (int e = 0; e < 4; ++e) {
         const uint32_t c = w[e];
         if (x + e < N) {
-          const uint32_t nc = c != EMPTY ? __ldg(fwd + (int64_t)(c >> 16) * N + (c & 0xFFFFu)) : EMPTY;
+          const uint32_t nc = c != EMPTY ? __ldg(fwd + c) : EMPTY;
           w[e] = nc;
           // (cy - y + 44, cx - x - e + 44); EMPTY is far
           mx = __vmaxu2(mx, nc == EMPTY ? 0xFFFFFFFFu : __vadd2(nc, __vsub2(nbx, (uint32_t)e)));
@@ -1858,7 +1891,7 @@ __global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, i
     uint32_t nc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      nc[e] = cur[e] != EMPTY ? __ldg(fwd + (int64_t)(cur[e] >> 16) * N + (cur[e] & 0xFFFFu)) : EMPTY;
+      nc[e] = cur[e] != EMPTY ? __ldg(fwd + cur[e]) : EMPTY;
     int r, x0;
     round_at(i, r, x0);
     uint32_t* row = g + (int64_t)r * pitch;

@@ -17,7 +17,7 @@
 #   variants  scripts/time_variants.py (build/variants/*.so)
 #   skab      A/B of the shared-term pass kernel (VD_NO_SK=1 vs 0), per-k pass times
 #   sweeps    scripts/sweep.py radius + density at 4096^2 (BASELINE configs[2])
-#   sanitize  compute-sanitizer memcheck/racecheck/synccheck/initcheck on scripts/sanitize_small.py
+#   sanitize  (closed on this pool since r02b) compute-sanitizer on scripts/sanitize_small.py
 set -x
 TAG=${TAG:-r02}
 mkdir -p gpurun_out
@@ -49,7 +49,8 @@ skab) timeout 900 python scripts/time_variants.py VD_NO_SK=1,0 2>&1 | tee gpurun
 envab) timeout 900 python scripts/time_variants.py $ENVAB 2>&1 | tee -a gpurun_out/envab_$TAG.txt ;;
 sweeps) timeout 900 python scripts/sweep.py --kind radius > gpurun_out/sweep_radius_$TAG.jsonl 2> gpurun_out/sweep_radius_$TAG.err
   timeout 900 python scripts/sweep.py --kind density > gpurun_out/sweep_density_$TAG.jsonl 2> gpurun_out/sweep_density_$TAG.err ;;
-sanitize) for tool in memcheck racecheck synccheck initcheck; do
+sanitize) echo "compute-sanitizer is closed on this GPU pool (r02b); use the VD_CHECK debug build (scripts/check_wsk_variant.py)"; continue
+  for tool in memcheck racecheck synccheck initcheck; do
     echo "# compute-sanitizer --tool $tool python scripts/sanitize_small.py ($TAG)" > gpurun_out/sanitizer_${tool}_$TAG.txt
     timeout 1200 compute-sanitizer --tool $tool python scripts/sanitize_small.py >> gpurun_out/sanitizer_${tool}_$TAG.txt 2>&1
     tail -3 gpurun_out/sanitizer_${tool}_$TAG.txt

@@ -47,3 +47,20 @@ for k in (1, 2, 4, 16, 512):
     d.jump_pass(k)
 print("windowed", hex(d.label_hash()), flush=True)
 d.close()
+
+# the wide exact pass (forced at small N by its test hook): JFA and passes with EMPTY, partial groups
+os.environ["VD_FORCE_WINDOWED"] = "0"
+os.environ["VD_FORCE_WSK"] = "1"
+for N in (1536, 2048):
+    xy = synth.uniform_seeds(N, N * N // 256, rng_seed=3)
+    d = vd.VoronoiDiagram(N, xy)
+    d.jfa()
+    rng = np.random.default_rng(N)
+    G = ((rng.integers(0, N, (N, N)) << 16) | rng.integers(0, N, (N, N))).astype(np.uint32)
+    G[rng.random((N, N)) < 0.5] = 0xFFFFFFFF
+    for k in (256, 512):
+        if 4 * k <= N:
+            d.set_labels(G)
+            d.jump_pass(k)
+    print("wide", N, hex(d.label_hash()), flush=True)
+    d.close()

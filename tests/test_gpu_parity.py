@@ -554,6 +554,40 @@ def test_single_pass_windowed_forced_bit_exact(vd, monkeypatch, N, metric, vn):
             assert np.array_equal(d.labels(), oracle.jump_pass(G, k, metric=metric, vn=vn)), (k, (G == EMPTY).any())
 
 
+# The wide exact pass (jump_pass_wsk, the kernel of JFA's large steps beyond N = 32768) forced at
+# small N by its test hook: its key arithmetic holds for any N <= 65536.  JFA (the virtual far
+# seed of N <= 16384 included), single passes on random maps with and without EMPTY, planted ties,
+# partial groups of 4k columns (1536, 2560) and ragged tensor-map cases (k not dividing N).
+@pytest.mark.parametrize("N", [1024, 1536, 2048, 2560, 4096])
+def test_wide_pass_forced_small_n_bit_exact(vd, monkeypatch, N):
+    monkeypatch.setenv("VD_FORCE_WSK", "1")
+    s = max(4, N * N // 256)
+    xy = synth.uniform_seeds(N, s, rng_seed=N + 3)
+    d = vd.VoronoiDiagram(N, xy)
+    d.jfa()
+    assert np.array_equal(d.labels(), oracle.jfa(N, xy))
+    rng = np.random.default_rng(N)
+    far = ((rng.integers(0, N, (N, N)) << 16) | rng.integers(0, N, (N, N))).astype(np.uint32)
+    ties = far.copy()
+    for y, x in rng.integers(300, N - 300, (2000, 2)):
+        a = int(rng.integers(0, 40))
+        ties[y, x] = far[0, 0]
+        ties[y, x - 256] = oracle.pack(x + a, y + 7)   # mirror labels about column x (same cy)
+        ties[y, x + 256] = oracle.pack(x - a, y + 7)
+        ties[y - 256, x] = oracle.pack(x + 3, y + 4)   # d2 = 25 vs 26 with the smaller cy
+        ties[y + 256, x] = oracle.pack(x + 1, y - 5)
+    holes = far.copy()
+    holes[rng.random((N, N)) < 0.7] = EMPTY
+    holes[: N // 3, : N // 3] = EMPTY
+    for G in (far, ties, holes):
+        for k in (256, 512, 1024):
+            if 4 * k <= N:
+                d.set_labels(G)
+                d.jump_pass(k)
+                assert np.array_equal(d.labels(), oracle.jump_pass(G, k)), (N, k, (G == EMPTY).any())
+    d.close()
+
+
 @pytest.mark.parametrize("G,metric,vn", [(4, "euclid", False), (8, "manhattan", False), (2, "euclid", True)])
 def test_virtual_shards_single_pass_bit_exact(vd, G, metric, vn):
     # Sharded passes with the halo exchange overlapped (interior rows, then the two edge
