@@ -185,6 +185,8 @@ struct vd_ctx {
   bool fuse_pack = false;                 // ... and may take the packed walk (previous flag + move bound)
   bool in_djfa = false;                   // passes of a vd_djfa_step are running
   bool hash_pass = false;                 // the running pass also accumulates the label checksum
+  bool rst_pending = false;               // fwd[rst_seeds[i]] <- EMPTY still to do (folded into the next jump_pass_sk)
+  const uint32_t* rst_seeds = nullptr;    // ... the old seed positions
   unsigned long long* counter_h = nullptr;   // pinned host copy
   uint32_t last_passes = 0;
   uint64_t launches = 0;
@@ -484,6 +486,9 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.fwd = nullptr;
   a.prefetch = 0;
   a.hash_out = nullptr;
+  a.rst_fwd = nullptr;
+  a.rst_seeds = nullptr;
+  a.rst_s = 0;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
   a.top = sh.top[h->hpar];
@@ -610,6 +615,12 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
                                                a.res_in_y ? (unsigned)a.segs : nres);
         e = vdl::launch_sk_remap(h->device, k, a, tm, g2, blk, sm, h->stream);
       } else {
+        if (h->rst_pending && !banded) {  // the fused frame's fwd reset, folded into this pass
+          a.rst_fwd = h->fwd;
+          a.rst_seeds = h->rst_seeds;
+          a.rst_s = (int64_t)h->s;
+          h->rst_pending = false;
+        }
         if (k == 1 && h->hash_pass && !may_empty) a.hash_out = h->counter;  // the frame's last pass also sums the checksum
         e = vdl::launch_sk(h->device, k, may_empty, banded, five, a.hash_out != nullptr, a, tm, grid, blk, sm, h->stream);
       }
@@ -1258,12 +1269,28 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
     st = run_pass(h, k1, false, false, ks.size() > 1 ? ks[1] : 0);
     h->fuse_remap = false;
     if (st) return loc_end(h), st;
-    vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, (int64_t)h->s);
-    if ((st = after_launch(h, "fwd_reset"))) return st;
+    // fwd back to all-EMPTY: folded into the second pass when it runs on jump_pass_sk (VD_NO_RST_FOLD=1:
+    // the separate fwd_reset kernel), else a kernel of its own
+    static const bool no_fold = [] { const char* e = getenv("VD_NO_RST_FOLD"); return e && e[0] == '1'; }();
+    h->rst_seeds = h->seeds;
+    h->rst_pending = !no_fold && ks.size() > 1;
     std::swap(h->seeds, h->seeds_new);
     for (size_t i = 1; i < ks.size(); ++i) {
       h->hash_pass = hash_fused && i + 1 == ks.size();
-      if ((st = run_pass(h, ks[i], false, false, i + 1 < ks.size() ? ks[i + 1] : 0))) return loc_end(h), st;
+      if ((st = run_pass(h, ks[i], false, false, i + 1 < ks.size() ? ks[i + 1] : 0))) {
+        h->rst_pending = false;
+        return loc_end(h), st;
+      }
+      if (h->rst_pending) {  // that pass could not carry it
+        h->rst_pending = false;
+        vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->rst_seeds, (int64_t)h->s);
+        if ((st = after_launch(h, "fwd_reset"))) return st;
+      }
+    }
+    if (h->rst_pending || ks.size() == 1 || no_fold) {  // no second pass (or the fold is off)
+      h->rst_pending = false;
+      vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->rst_seeds, (int64_t)h->s);
+      if ((st = after_launch(h, "fwd_reset"))) return st;
     }
     loc_end(h);
     h->last_passes = (uint32_t)ks.size();

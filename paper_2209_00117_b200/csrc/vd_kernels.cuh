@@ -51,6 +51,11 @@ struct PassArgs {
   const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label)
   int32_t prefetch;     // jump_pass_sk_remap: also pull the fwd lines of the row after next into L1
   unsigned long long* hash_out;  // jump_pass_sk<1> HASH: add the outputs' label checksum here
+  // jump_pass_sk: also restore fwd[rst_seeds[i]] = EMPTY for i < rst_s (the fused dJFA frame's
+  // fwd reset, folded into its second pass: a few scattered stores per CTA, hidden behind staging)
+  uint32_t* rst_fwd;
+  const uint32_t* rst_seeds;
+  int64_t rst_s;
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
@@ -1222,9 +1227,17 @@ __host__ __device__ constexpr int ilog2_c(int v) { return v <= 1 ? 0 : 1 + ilog2
 // groups of a.nwalk residue classes.  Host: N % 512 == 0, k a power of two, k <= N / 4;
 // Euclidean Moore passes, no window (N <= 32768).  KM: k itself for k <= 4096 (compile-time
 // step), 8192 for any larger k.
+__device__ __forceinline__ void folded_fwd_reset(const PassArgs& a) {
+  if (a.rst_fwd == nullptr) return;
+  const int64_t nb = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+  const int64_t b = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
+  for (int64_t i = b * blockDim.x + threadIdx.x; i < a.rst_s; i += nb * blockDim.x) a.rst_fwd[a.rst_seeds[i]] = EMPTY;
+}
+
 template <int KM, bool MAY_EMPTY, bool BANDED, bool HASH = false, int MINB = VD_MIN_BLOCKS>
 __global__ void __launch_bounds__(kThreads, MINB) jump_pass_sk(PassArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint32_t dyn_smem[];
+  folded_fwd_reset(a);
   const int xb = (int)blockIdx.x;
   const bool full = a.nwalk > 0;
   const int seg = full ? 0 : (int)(a.res_in_y ? blockIdx.z : blockIdx.y);
