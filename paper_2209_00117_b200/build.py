@@ -9,8 +9,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 # vd.cu (host runtime + C ABI + the non-pass kernels) and one translation unit per jump-pass
 # kernel family (vd_launch_*.cu), compiled in parallel and linked into one shared library
-SRC = [os.path.join(PKG, "csrc", f) for f in ("vd.cu", "vd_launch_sk_small.cu", "vd_launch_sk_mid.cu",
-                                               "vd_launch_sk_large.cu", "vd_launch_remap.cu", "vd_launch_fast.cu",
+SRC = [os.path.join(PKG, "csrc", f) for f in ("vd.cu", "vd_launch_sk_small_a.cu", "vd_launch_sk_small_b.cu",
+                                               "vd_launch_sk_mid_a.cu", "vd_launch_sk_mid_b.cu", "vd_launch_sk_large_a.cu",
+                                               "vd_launch_sk_large_b.cu", "vd_launch_remap.cu", "vd_launch_fast.cu",
                                                "vd_launch_wide.cu", "vd_launch_wsk.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "vd_kernels.cuh"), os.path.join(PKG, "csrc", "vd_launch.h"),
               os.path.join(ROOT, "include", "vd.h")]

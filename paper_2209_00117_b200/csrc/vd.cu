@@ -185,6 +185,7 @@ struct vd_ctx {
   bool fuse_pack = false;                 // ... and may take the packed walk (previous flag + move bound)
   bool in_djfa = false;                   // passes of a vd_djfa_step are running
   bool hash_pass = false;                 // the running pass also accumulates the label checksum
+  bool lat_pass = false;                  // the running pass belongs to vd_jfa's schedule (lattice invariant holds)
   bool rst_pending = false;               // fwd[rst_seeds[i]] <- EMPTY still to do (folded into the next jump_pass_sk)
   const uint32_t* rst_seeds = nullptr;    // ... the old seed positions
   unsigned long long* counter_h = nullptr;   // pinned host copy
@@ -477,6 +478,7 @@ struct Push {  // where a launch also stores the rows the neighbours' next pass 
   uint32_t k = 0;
 };
 
+uint32_t unclaimed_label(const vd_ctx* h);
 vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn, int64_t y_lo = -1,
                       int64_t y_hi = -1, const Push* push = nullptr) {
   vdk::PassArgs a;
@@ -489,6 +491,10 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.rst_fwd = nullptr;
   a.rst_seeds = nullptr;
   a.rst_s = 0;
+  a.lat = 0;
+  a.lat_empty = VD_EMPTY;
+  a.lat_min = h->N < 65536 ? h->N << 16 : VD_EMPTY;
+  a.lat_vl = 0;
   a.in = sh.buf[h->cur];
   a.out = sh.buf[h->cur ^ 1];
   a.top = sh.top[h->hpar];
@@ -524,7 +530,28 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   a.y_hi = (int)y_hi;
   const uint32_t R = (uint32_t)(y_hi - y_lo);  // output rows of this launch
   if (R == 0) return VD_OK;
-  const bool sk = sk_ok(h, k, vn, may_empty) && (k & (k - 1)) == 0;
+  // JFA's lattice walk (jump_pass_sk LAT): a pass of vd_jfa's schedule (its input congruent to the
+  // pixels mod 2k), Euclidean Moore, stride step k >= 4; lattice coordinates below 64 (N <= 64k), or
+  // below 128 once no EMPTY is left (N <= 128k, the packed key's range).  Beyond N = 32768 only, where
+  // it replaces the wide pass; below, the 32-bit exact walk is as fast (measured).
+  // VD_NO_LAT=1 disables it, VD_LAT_ALL=1 also takes N <= 32768 (A/B).
+  static const bool no_lat = [] { const char* e = getenv("VD_NO_LAT"); return e && e[0] == '1'; }();
+  static const bool lat_all = [] { const char* e = getenv("VD_LAT_ALL"); return e && e[0] == '1'; }();
+  uint32_t lk = 0;
+  while ((1u << lk) < k) ++lk;
+  const uint32_t lmax = (h->N - 1) >> lk;  // largest lattice coordinate
+  const bool lat_geo = !no_lat && h->lat_pass && !vn && h->metric == 0 && (k & (k - 1)) == 0 && k >= 4 &&
+                       4 * k <= h->N && h->N % 512 == 0 && !h->force_rel && (h->N > 32768 || lat_all);
+  const bool no_unclaimed = !may_empty && h->N > 16384;  // (N <= 16384 runs on the virtual far seed)
+  // 3: the exact 32-bit walk in lattice units (lattice coordinates < 2^14 for k >= 4), with the
+  // unclaimed labels at (2L+1, 2L+1) like the virtual far seed; VD_NO_LATX=1 disables it (A/B)
+  static const bool no_latx = [] { const char* e = getenv("VD_NO_LATX"); return e && e[0] == '1'; }();
+  // (lat 3 only for k >= 256, where it replaces the wide pass: 12.3 -> 9.6 ms at C5's k = 256; for
+  // k <= 128 the windowed walk stays, 0.3 ms faster, `profiles/r02c_latx_ab_c5.txt`)
+  const int lat_kind = !lat_geo ? 0 : lmax <= 63 ? (no_unclaimed ? 2 : 1) : (lmax <= 127 && no_unclaimed) ? 2
+                                                 : (no_latx || k < 256) ? 0 : 3;
+  const bool lat = lat_kind > 0;
+  const bool sk = lat || (sk_ok(h, k, vn, may_empty) && (k & (k - 1)) == 0);
   const bool wsk = !sk && wsk_ok(h, k, vn);
   const bool rel = !sk && !wsk && (rel_ok(h->N, may_empty, k) || (h->force_rel && !may_empty && k <= 4096));
   if ((sk || wsk || fast_ok(h->N, may_empty) || rel) && (k & (k - 1)) == 0) {
@@ -622,7 +649,13 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
           h->rst_pending = false;
         }
         if (k == 1 && h->hash_pass && !may_empty) a.hash_out = h->counter;  // the frame's last pass also sums the checksum
-        e = vdl::launch_sk(h->device, k, may_empty, banded, five, a.hash_out != nullptr, a, tm, grid, blk, sm, h->stream);
+        if (lat) {
+          a.lat = lat_kind;
+          a.lat_empty = unclaimed_label(h);
+          a.lat_vl = ((2 * lmax + 1) << 16) | (2 * lmax + 1);
+        }
+        e = vdl::launch_sk(h->device, k, may_empty && !lat, banded, five, a.hash_out != nullptr, a, tm, grid, blk, sm,
+                           h->stream);
       }
     } else {
       e = vdl::launch_fast(h->device, k, may_empty, banded, rel, h->metric, vn, a, grid, blk, sm, h->stream);
@@ -1149,7 +1182,11 @@ vd_status vd_jfa(vd_handle h) {
     // JFA's labels are still far from their pixels at large steps: there the windowed kernel
     // would recompute most walks, and the 64-bit one is cheaper (C5: 31 vs 68 ms at k = 512).
     const bool far = h->N > 32768 && ks[i] > 256 && !wsk_ok(h, ks[i], vn);
+    // the passes of the schedule proper (not the extra k = 1 passes) keep every label congruent to
+    // its pixel mod the step: the lattice walk may take them
+    h->lat_pass = i < ks.size() - h->extras;
     st = run_pass(h, ks[i], may_empty || far, vn, i + 1 < ks.size() ? ks[i + 1] : 0);
+    h->lat_pass = false;
     h->track_empty = false;
     if (st) return loc_end(h), st;
     if (track && may_empty) {

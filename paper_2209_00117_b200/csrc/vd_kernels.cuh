@@ -56,6 +56,13 @@ struct PassArgs {
   uint32_t* rst_fwd;
   const uint32_t* rst_seeds;
   int64_t rst_s;
+  // jump_pass_sk LAT (JFA's steps with N <= 64k): every input label is congruent to its pixel mod 2k,
+  // so candidates are evaluated in lattice units (coordinate >> log2 k) by the packed walk; EMPTY and
+  // the virtual far seed map to the lattice point (127, 127); lat_empty = the unclaimed label to output
+  int32_t lat;         // 0 off, 1 lattice walk with unclaimed labels possible, 2 none possible
+  uint32_t lat_empty;  // the unclaimed label (EMPTY, or the virtual far seed)
+  uint32_t lat_min;    // labels >= lat_min are unclaimed (N << 16, or EMPTY at N = 65536)
+  uint32_t lat_vl;     // lat 3: the lattice stand-in for unclaimed labels, (2L+1, 2L+1) for lattice size L
   uint32_t vempty;  // in-kernel stand-in for EMPTY (MAY_EMPTY variant), see jump_pass_fast
   uint32_t sh16;    // 65536 (a run-time value on purpose)
   uint32_t one;     // 1 (a run-time value on purpose: keeps x*1+y an IMAD on the FMA pipe)
@@ -965,8 +972,17 @@ __device__ __forceinline__ uint32_t ld_fwd(const uint32_t* p, uint64_t pol) {
 #define VD_FUSE_LA 1  // rows of fwd-gather look-ahead in the fused remap pass (1 or 2)
 #endif
 constexpr int kFuseLA = VD_FUSE_LA;
+// LAT (with PACK, stride steps): the JFA lattice walk.  After passes N/2 .. 2k of a JFA every label
+// is congruent to its pixel mod 2k (the first pass takes seeds at p + o k1; a pass k takes a label of
+// p + o k), so every candidate of pass k lies at (dx, dy) = k (a, b) with integers a, b, and
+// (d2, c) orders as (a^2 + b^2, b, a).  In lattice coordinates (>> log2 k) that is the packed key
+// with (a, b) for (dx, dy): exact when N <= 64 k (|a|, |b| <= 63).  EMPTY and the virtual far seed go
+// to the lattice point (127, 127): at least 64 units from every pixel, so they lose to every real
+// label, and an output decoded as (127, 127) had only such candidates.  The output is the lattice
+// label scaled back, (o << log2 k) | (y mod k, X mod k).
+constexpr uint32_t kLatEmpty = (127u << 16) | 127u;
 template <int KM, bool MAY_EMPTY, bool BANDED, bool FIX, bool PACK, bool FULL, bool REMAP = false, bool PRE = false,
-          bool X64 = false, bool HASH = false>
+          bool X64 = false, bool HASH = false, int LAT = 0>
 __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm, int x0, int X, int y0,
                                         uint32_t* smem) {
   constexpr int KS = KM < kVec ? KM : 1;
@@ -987,17 +1003,21 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
 
   if constexpr (!PRE) stage_walk<FULL, BANDED>(a, tm, x0, y0, k, nout, nlist, spans, K4, SE, smem, bars);
 
-  // per-thread slot offsets in a stage, columns, and edge flags
+  // per-thread slot offsets in a stage, columns, and edge flags.  The key arithmetic runs on
+  // (Xa, ka): the columns and step themselves, or (LAT) their lattice units X >> log2 k and 1
+  static_assert(LAT == 0 || (STRIDE && PACK == (LAT < 3)), "lattice walks: packed (1, 2) or exact (3), stride steps");
+  const int ka = LAT ? 1 : k;
+  const int Xa = LAT ? (X >> a.lk) : X;
   const uint32_t sh16 = a.sh16;
   int xs_home[NS], xs_out[kVec];
   constexpr uint32_t P1 = PACK ? 1u : 0u;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    const int col = STRIDE ? X + (s - 1) * k : X + s - KS;
+    const int col = STRIDE ? Xa + (s - 1) * ka : X + s - KS;
     xs_home[s] = (int)(P1 - ((uint32_t)col << 16));
   }
 #pragma unroll
-  for (int e = 0; e < kVec; ++e) xs_out[e] = (int)(P1 - ((uint32_t)(STRIDE ? X + e * k : X + e) << 16));
+  for (int e = 0; e < kVec; ++e) xs_out[e] = (int)(P1 - ((uint32_t)(STRIDE ? Xa + e * ka : X + e) << 16));
   const bool left_out = FIX && (STRIDE ? X - k < 0 : X - KS < 0);
   const bool right_out = FIX && (STRIDE ? X + 4 * k >= N : X + 3 + KS >= N);
   // stride: slot s (column X + (s-1) k) lies in the grid iff s - 1 < nc, output e iff e < nc.  With
@@ -1006,9 +1026,10 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   const int nc = (STRIDE && FIX) ? (X >= N ? 0 : ((N - 1 - X) >> a.lk) + 1) : 8;
   int xb[kVec];
 #pragma unroll
-  for (int e = 0; e < kVec; ++e) xb[e] = (STRIDE ? X + e * k : X + e) - 128;
+  for (int e = 0; e < kVec; ++e) xb[e] = (STRIDE ? Xa + e * ka : X + e) - 128;
   // constants (uniform): exact (k^2, 2k); packed (k^2 2^16 - k, k^2 2^16 + k, 2k 2^16)
-  const uint32_t uk = (uint32_t)k;
+  const uint32_t uk = (uint32_t)ka;
+  bool any_e = false;  // LAT: some output stayed unclaimed
   const uint32_t k2 = PACK ? uk * uk * 65536u - uk : uk * uk;
   const uint32_t m1 = PACK ? uk * uk * 65536u + uk : 2u * uk;
   const uint32_t m3 = 2u * uk * 65536u;
@@ -1079,6 +1100,23 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         for (int s = 4 + KS; s < NS; ++s) lab[s] = right_out ? lab[s - KS] : lab[s];
       }
     }
+    if constexpr (LAT > 0) {  // labels to lattice coordinates (both 16-bit halves >> log2 k)
+      const uint32_t msk = (0xFFFFu >> a.lk) * 0x10001u;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t c = lab[s];
+        // LAT 1: EMPTY / the virtual far seed (labels at or beyond row N: c >= a.lat_min) -> (127, 127)
+        const bool E = LAT == 1 && c >= a.lat_min;
+#ifdef VD_CHECK  // the lattice invariant (debug builds): label = pixel (mod k) in both coordinates
+        if (!(c == EMPTY || c == a.lat_empty) &&
+            ((((c & 0xFFFFu) - (uint32_t)X) | ((c >> 16) - (uint32_t)y0)) & (uint32_t)(k - 1)) != 0u)
+          __trap();
+        if (LAT == 2 && (c == EMPTY || c == a.lat_empty)) __trap();
+#endif
+        const bool E3 = LAT == 3 && c >= a.lat_min;
+        lab[s] = E ? kLatEmpty : E3 ? a.lat_vl : ((c >> a.lk) & msk);
+      }
+    }
     build_sk<KS, MAY_EMPTY, PACK>(lab, xs_home, xs_out, a.vempty, sh16, k2, m1, 0u, m3, R);
   };
 
@@ -1114,7 +1152,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         for (int e = 0; e < kVec; ++e) o[e] = best64_sk<KS>(Pv, Cv, Nx, e, STRIDE ? X + e * k : X + e, y);
         loc_bad = true;  // not tracked on this path
       } else if constexpr (PACK) {
-        const uint32_t uy = (uint32_t)y;
+        const uint32_t uy = LAT > 0 ? (uint32_t)(y >> a.lk) : (uint32_t)y;
         const uint32_t My = 256u - (uy << 17);
         const uint32_t Cy = uy * uy * 65536u - 256u * uy + 32896u;
         const uint32_t Yb = (uy - 128u) << 16;
@@ -1128,7 +1166,32 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         }
 #pragma unroll
         for (int e = 0; e < kVec; ++e) o[e] = __byte_perm(sk[e], 0u, 0x4140) + Yb + (uint32_t)xb[e];
-        loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
+        if constexpr (LAT > 0) {  // lattice label -> label: (o << log2 k) | (y mod k, X mod k)
+          const uint32_t low = ((uint32_t)(y & (k - 1)) << 16) | (uint32_t)(X & (k - 1));
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            if constexpr (LAT == 1) {
+              const bool E = o[e] == kLatEmpty;
+              any_e |= E;
+              o[e] = E ? a.lat_empty : ((o[e] << a.lk) | low);
+            } else {
+              o[e] = (o[e] << a.lk) | low;
+            }
+          }
+        } else {
+          loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
+        }
+      } else if constexpr (LAT == 3) {  // exact walk in lattice units (any N <= 65536 with k >= 4)
+        const int ye = y >> a.lk;
+        const uint32_t low = ((uint32_t)(y & (k - 1)) << 16) | (uint32_t)(X & (k - 1));
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          int me;
+          const uint32_t v = best_sk<KS>(Pv, Cv, Nx, e, ye, me);
+          const bool E = v == a.lat_vl;
+          any_e |= E;
+          o[e] = E ? a.lat_empty : ((v << a.lk) | low);
+        }
       } else {
         int mm = -0x7FFFFFFF - 1;
 #pragma unroll
@@ -1211,9 +1274,13 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
   }
   if (a.loc_out) {
     bool far;
-    if constexpr (PACK) far = loc_acc >= ((kLocD2 + 1u) << 16);
+    if constexpr (LAT > 0) far = true;  // (locality is not tracked in lattice units)
+    else if constexpr (PACK) far = loc_acc >= ((kLocD2 + 1u) << 16);
     else far = loc_bad;
     if (__syncthreads_or(far) && tid == 0) atomicOr(a.loc_out, 1u);
+  }
+  if constexpr (LAT == 1 || LAT == 3) {
+    if (a.empty_flag != nullptr && __syncthreads_or(any_e) && tid == 0) atomicOr(a.empty_flag, 1ull);
   }
   if constexpr (HASH) {
     const uint64_t t = block_sum_u64(hacc);
@@ -1262,6 +1329,39 @@ __global__ void __launch_bounds__(kThreads, MINB) jump_pass_sk(PassArgs a, const
     X = x0 + tid;
     fix = g == 0 || x0 + 4 * k + 128 > a.N;  // some right neighbour column (X + 4k) beyond the grid
     if (x0 >= a.N) return;  // (the partial last group of a grid that is not a multiple of 4k)
+  }
+  if constexpr (KM >= kVec && !MAY_EMPTY && MINB == VD_MIN_BLOCKS && !HASH) {
+    // JFA's lattice walk: 1 = unclaimed labels possible (N <= 64k), 2 = none left (N <= 128k)
+    if (a.lat == 1) {
+      if (full) {
+        if (fix) walk_sk<KM, false, BANDED, true, true, true, false, false, false, false, 1>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, true, true, false, false, false, false, 1>(a, &tm, x0, X, y0, dyn_smem);
+      } else {
+        if (fix) walk_sk<KM, false, BANDED, true, true, false, false, false, false, false, 1>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, true, false, false, false, false, false, 1>(a, &tm, x0, X, y0, dyn_smem);
+      }
+      return;
+    }
+    if (a.lat == 3) {
+      if (full) {
+        if (fix) walk_sk<KM, false, BANDED, true, false, true, false, false, false, false, 3>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, false, true, false, false, false, false, 3>(a, &tm, x0, X, y0, dyn_smem);
+      } else {
+        if (fix) walk_sk<KM, false, BANDED, true, false, false, false, false, false, false, 3>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, false, false, false, false, false, false, 3>(a, &tm, x0, X, y0, dyn_smem);
+      }
+      return;
+    }
+    if (a.lat == 2) {
+      if (full) {
+        if (fix) walk_sk<KM, false, BANDED, true, true, true, false, false, false, false, 2>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, true, true, false, false, false, false, 2>(a, &tm, x0, X, y0, dyn_smem);
+      } else {
+        if (fix) walk_sk<KM, false, BANDED, true, true, false, false, false, false, false, 2>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, true, false, false, false, false, false, 2>(a, &tm, x0, X, y0, dyn_smem);
+      }
+      return;
+    }
   }
   if (full) {  // JFA's large steps: exact walk (their diagrams are never local)
     if (fix) walk_sk<KM, MAY_EMPTY, BANDED, true, false, true, false, false, false, HASH>(a, &tm, x0, X, y0, dyn_smem);

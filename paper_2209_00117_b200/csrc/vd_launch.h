@@ -22,18 +22,27 @@ cudaError_t launch_fast(int dev, uint32_t k, bool me, bool bd, bool rel, int met
 
 // jump_pass_sk (Euclidean Moore, shared terms): power-of-two k.  five = dJFA's 5-CTA/SM
 // instantiation (4 <= k <= 64, no EMPTY); hash = the checksum-summing k = 1 pass.
-// Split by k range over three TUs: k <= 16, 32 <= k <= 256, k >= 512.
-cudaError_t launch_sk_small(int dev, uint32_t k, bool me, bool bd, bool five, bool hash, const vdk::PassArgs& a,
+// Split by k range over six TUs (vd_launch_sk_{small,mid,large}_{a,b}.cu).
+cudaError_t launch_sk_small_a(int dev, uint32_t k, bool me, bool bd, bool five, bool hash, const vdk::PassArgs& a,
+                              const CUtensorMap& tm, dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
+cudaError_t launch_sk_small_b(int dev, uint32_t k, bool me, bool bd, bool five, bool hash, const vdk::PassArgs& a,
+                              const CUtensorMap& tm, dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
+cudaError_t launch_sk_mid_a(int dev, uint32_t k, bool me, bool bd, bool five, const vdk::PassArgs& a,
                             const CUtensorMap& tm, dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
-cudaError_t launch_sk_mid(int dev, uint32_t k, bool me, bool bd, bool five, const vdk::PassArgs& a,
-                          const CUtensorMap& tm, dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
-cudaError_t launch_sk_large(int dev, uint32_t k, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm,
-                            dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
+cudaError_t launch_sk_mid_b(int dev, uint32_t k, bool me, bool bd, bool five, const vdk::PassArgs& a,
+                            const CUtensorMap& tm, dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
+cudaError_t launch_sk_large_a(int dev, uint32_t k, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm,
+                              dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
+cudaError_t launch_sk_large_b(int dev, uint32_t k, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm,
+                              dim3 grid, dim3 blk, size_t smem, cudaStream_t st);
 inline cudaError_t launch_sk(int dev, uint32_t k, bool me, bool bd, bool five, bool hash, const vdk::PassArgs& a,
                              const CUtensorMap& tm, dim3 grid, dim3 blk, size_t smem, cudaStream_t st) {
-  if (k <= 16) return launch_sk_small(dev, k, me, bd, five, hash, a, tm, grid, blk, smem, st);
-  if (k <= 256) return launch_sk_mid(dev, k, me, bd, five, a, tm, grid, blk, smem, st);
-  return launch_sk_large(dev, k, me, bd, a, tm, grid, blk, smem, st);
+  if (k <= 2) return launch_sk_small_a(dev, k, me, bd, five, hash, a, tm, grid, blk, smem, st);
+  if (k <= 16) return launch_sk_small_b(dev, k, me, bd, five, hash, a, tm, grid, blk, smem, st);
+  if (k <= 64) return launch_sk_mid_a(dev, k, me, bd, five, a, tm, grid, blk, smem, st);
+  if (k <= 256) return launch_sk_mid_b(dev, k, me, bd, five, a, tm, grid, blk, smem, st);
+  if (k <= 1024) return launch_sk_large_a(dev, k, me, bd, a, tm, grid, blk, smem, st);
+  return launch_sk_large_b(dev, k, me, bd, a, tm, grid, blk, smem, st);
 }
 
 // jump_pass_sk_remap (first dJFA pass with the remap fused in): 4 <= k <= 128.

@@ -4,14 +4,12 @@
 
 namespace vdl {
 
-cudaError_t launch_sk_large(int dev, uint32_t k, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm,
+cudaError_t launch_sk_large_a(int dev, uint32_t k, bool me, bool bd, const vdk::PassArgs& a, const CUtensorMap& tm,
                             dim3 g, dim3 b, size_t sm, cudaStream_t st) {
   switch (k) {
     case 512: return sk_k<512>(dev, me, bd, a, tm, g, b, sm, st);
     case 1024: return sk_k<1024>(dev, me, bd, a, tm, g, b, sm, st);
-    case 2048: return sk_k<2048>(dev, me, bd, a, tm, g, b, sm, st);
-    case 4096: return sk_k<4096>(dev, me, bd, a, tm, g, b, sm, st);
-    default: return sk_k<8192>(dev, me, bd, a, tm, g, b, sm, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 

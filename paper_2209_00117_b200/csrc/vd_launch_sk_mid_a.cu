@@ -3,13 +3,11 @@
 
 namespace vdl {
 
-cudaError_t launch_sk_mid(int dev, uint32_t k, bool me, bool bd, bool five, const vdk::PassArgs& a,
+cudaError_t launch_sk_mid_a(int dev, uint32_t k, bool me, bool bd, bool five, const vdk::PassArgs& a,
                           const CUtensorMap& tm, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
   switch (k) {
     case 32: return sk_k5<32>(dev, me, bd, five, a, tm, g, b, sm, st);
     case 64: return sk_k5<64>(dev, me, bd, five, a, tm, g, b, sm, st);
-    case 128: return sk_k<128>(dev, me, bd, a, tm, g, b, sm, st);
-    case 256: return sk_k<256>(dev, me, bd, a, tm, g, b, sm, st);
     default: return cudaErrorInvalidValue;
   }
 }

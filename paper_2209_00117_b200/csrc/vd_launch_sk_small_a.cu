@@ -3,7 +3,7 @@
 
 namespace vdl {
 
-cudaError_t launch_sk_small(int dev, uint32_t k, bool me, bool bd, bool five, bool hash, const vdk::PassArgs& a,
+cudaError_t launch_sk_small_a(int dev, uint32_t k, bool me, bool bd, bool five, bool hash, const vdk::PassArgs& a,
                             const CUtensorMap& tm, dim3 g, dim3 b, size_t sm, cudaStream_t st) {
   switch (k) {
     case 1:
@@ -11,9 +11,6 @@ cudaError_t launch_sk_small(int dev, uint32_t k, bool me, bool bd, bool five, bo
         return bd ? sk_one<1, false, true, true>(dev, a, tm, g, b, sm, st) : sk_one<1, false, false, true>(dev, a, tm, g, b, sm, st);
       return sk_k<1>(dev, me, bd, a, tm, g, b, sm, st);
     case 2: return sk_k<2>(dev, me, bd, a, tm, g, b, sm, st);
-    case 4: return sk_k5<4>(dev, me, bd, five, a, tm, g, b, sm, st);
-    case 8: return sk_k5<8>(dev, me, bd, five, a, tm, g, b, sm, st);
-    case 16: return sk_k5<16>(dev, me, bd, five, a, tm, g, b, sm, st);
     default: return cudaErrorInvalidValue;
   }
 }
