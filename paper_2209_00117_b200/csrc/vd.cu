@@ -548,8 +548,11 @@ vd_status launch_pass(vd_ctx* h, Shard& sh, uint32_t k, bool may_empty, bool vn,
   static const bool no_latx = [] { const char* e = getenv("VD_NO_LATX"); return e && e[0] == '1'; }();
   // (lat 3 only for k >= 256, where it replaces the wide pass: 12.3 -> 9.6 ms at C5's k = 256; for
   // k <= 128 the windowed walk stays, 0.3 ms faster, `profiles/r02c_latx_ab_c5.txt`)
+  // 4: the same without unclaimed labels (C5's k = 128 ... 4 once EMPTY is gone; VD_NO_LAT4=1: the
+  // windowed walk there instead, A/B)
+  static const bool no_lat4 = [] { const char* e = getenv("VD_NO_LAT4"); return e && e[0] == '1'; }();
   const int lat_kind = !lat_geo ? 0 : lmax <= 63 ? (no_unclaimed ? 2 : 1) : (lmax <= 127 && no_unclaimed) ? 2
-                                                 : (no_latx || k < 256) ? 0 : 3;
+                     : no_latx ? 0 : (no_unclaimed && !no_lat4) ? 4 : k >= 256 ? 3 : 0;
   const bool lat = lat_kind > 0;
   const bool sk = lat || (sk_ok(h, k, vn, may_empty) && (k & (k - 1)) == 0);
   const bool wsk = !sk && wsk_ok(h, k, vn);

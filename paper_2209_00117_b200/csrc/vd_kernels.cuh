@@ -1005,7 +1005,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
 
   // per-thread slot offsets in a stage, columns, and edge flags.  The key arithmetic runs on
   // (Xa, ka): the columns and step themselves, or (LAT) their lattice units X >> log2 k and 1
-  static_assert(LAT == 0 || (STRIDE && PACK == (LAT < 3)), "lattice walks: packed (1, 2) or exact (3), stride steps");
+  static_assert(LAT == 0 || (STRIDE && PACK == (LAT < 3)), "lattice walks: packed (1, 2) or exact (3, 4), stride steps");
   const int ka = LAT ? 1 : k;
   const int Xa = LAT ? (X >> a.lk) : X;
   const uint32_t sh16 = a.sh16;
@@ -1111,7 +1111,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         if (!(c == EMPTY || c == a.lat_empty) &&
             ((((c & 0xFFFFu) - (uint32_t)X) | ((c >> 16) - (uint32_t)y0)) & (uint32_t)(k - 1)) != 0u)
           __trap();
-        if (LAT == 2 && (c == EMPTY || c == a.lat_empty)) __trap();
+        if ((LAT == 2 || LAT == 4) && (c == EMPTY || c == a.lat_empty)) __trap();
 #endif
         const bool E3 = LAT == 3 && c >= a.lat_min;
         lab[s] = E ? kLatEmpty : E3 ? a.lat_vl : ((c >> a.lk) & msk);
@@ -1181,16 +1181,20 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
         } else {
           loc_acc = __vimax3_u32(__vimax3_u32(loc_acc, sk[0], sk[1]), sk[2], sk[3]);
         }
-      } else if constexpr (LAT == 3) {  // exact walk in lattice units (any N <= 65536 with k >= 4)
+      } else if constexpr (LAT >= 3) {  // exact walk in lattice units (any N <= 65536 with k >= 4)
         const int ye = y >> a.lk;
         const uint32_t low = ((uint32_t)(y & (k - 1)) << 16) | (uint32_t)(X & (k - 1));
 #pragma unroll
         for (int e = 0; e < kVec; ++e) {
           int me;
           const uint32_t v = best_sk<KS>(Pv, Cv, Nx, e, ye, me);
-          const bool E = v == a.lat_vl;
-          any_e |= E;
-          o[e] = E ? a.lat_empty : ((v << a.lk) | low);
+          if constexpr (LAT == 3) {
+            const bool E = v == a.lat_vl;
+            any_e |= E;
+            o[e] = E ? a.lat_empty : ((v << a.lk) | low);
+          } else {  // 4: no unclaimed label can be present
+            o[e] = (v << a.lk) | low;
+          }
         }
       } else {
         int mm = -0x7FFFFFFF - 1;
@@ -1349,6 +1353,16 @@ __global__ void __launch_bounds__(kThreads, MINB) jump_pass_sk(PassArgs a, const
       } else {
         if (fix) walk_sk<KM, false, BANDED, true, false, false, false, false, false, false, 3>(a, &tm, x0, X, y0, dyn_smem);
         else walk_sk<KM, false, BANDED, false, false, false, false, false, false, false, 3>(a, &tm, x0, X, y0, dyn_smem);
+      }
+      return;
+    }
+    if (a.lat == 4) {
+      if (full) {
+        if (fix) walk_sk<KM, false, BANDED, true, false, true, false, false, false, false, 4>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, false, true, false, false, false, false, 4>(a, &tm, x0, X, y0, dyn_smem);
+      } else {
+        if (fix) walk_sk<KM, false, BANDED, true, false, false, false, false, false, false, 4>(a, &tm, x0, X, y0, dyn_smem);
+        else walk_sk<KM, false, BANDED, false, false, false, false, false, false, false, 4>(a, &tm, x0, X, y0, dyn_smem);
       }
       return;
     }
