@@ -168,6 +168,7 @@ struct vd_ctx {
   cudaEvent_t halo_ready = nullptr, halo_done = nullptr;
   cudaEvent_t copy_done = nullptr;
   uint32_t* fwd = nullptr;        // [N*N] forward map (dJFA), allocated on first use
+  uint32_t* bits = nullptr;       // [N * ceil(N/32)] seed bitmap of JFA's first pass, allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
   // Locality flags of one frame (packed-key pass, vd_kernels.cuh): loc[i] = 0 iff every label
   // of the input of the frame's i-th tracked pass lies within kLocR of its pixel.
@@ -875,6 +876,7 @@ void free_all(vd_ctx* h) {
   cudaFree(h->disp_buf[0]);
   cudaFree(h->disp_buf[1]);
   cudaFree(h->fwd);
+  cudaFree(h->bits);
   cudaFree(h->counter);
   cudaFree(h->loc);
 
@@ -1141,6 +1143,27 @@ namespace {
 // pass; needs no halo exchange (every rank holds every seed).
 vd_status jfa_init_first_pass(vd_ctx* h, uint32_t k1, bool vn) {
   const uint32_t u = unclaimed_label(h);
+  // VD_FIRST_GATHER=1: a gather from a seed bitmap instead of the scatter (k_1 >= 32; measured slower:
+  // C4 JFA 7.19 vs 6.62 ms, C5 135.5 vs 134.2 ms, `profiles/r02c_first_gather_ab_*.txt`)
+  static const bool gather = [] { const char* e = getenv("VD_FIRST_GATHER"); return e && e[0] == '1'; }();
+  if (gather && k1 >= 32) {
+    const int64_t wpr = (h->N + 31) / 32;
+    const size_t bytes = (size_t)h->N * wpr * sizeof(uint32_t);
+    if (!h->bits) CK(cudaMalloc(&h->bits, bytes));
+    CK(cudaMemsetAsync(h->bits, 0, bytes, h->stream));
+    vdk::seed_bits<<<grid_for(h, (int64_t)h->s, 256), 256, 0, h->stream>>>(h->bits, wpr, h->seeds, (int64_t)h->s);
+    vd_status st = after_launch(h, "seed_bits");
+    if (st) return st;
+    for (auto& sh : h->shards) {
+      vdk::jfa_first_gather<<<grid_for(h, (int64_t)sh.rows * wpr, 256), 256, 0, h->stream>>>(
+          sh.buf[h->cur], h->pitch, (int)sh.row0, (int)sh.rows, (int)h->N, (int)k1, h->bits, wpr, u, vn ? 1 : 0);
+      if ((st = after_launch(h, "jfa_first_gather"))) return st;
+    }
+    ++h->pass_seq;
+    h->hpar ^= 1;
+    h->pushed_k = 0;
+    return VD_OK;
+  }
   for (auto& sh : h->shards) {
     const int64_t n4 = (int64_t)sh.rows * h->pitch / 4;
     vdk::fill_value<<<grid_for(h, n4, 256), 256, 0, h->stream>>>(reinterpret_cast<uint4*>(sh.buf[h->cur]), n4, u);

@@ -1874,6 +1874,50 @@ __global__ void jfa_first_pass(uint32_t* __restrict__ g, int64_t pitch, int row0
   }
 }
 
+// JFA's first pass as a gather from a seed bitmap (r02c): bits[y * wpr + x / 32] bit x % 32 = a seed
+// at (x, y).  Pass k_1 gives pixel p the best seed among p + o k_1 (Table 1); since a seed's label is
+// its position, the key (d2, c) of an offset o depends on o alone, and the nine offsets have a fixed
+// order for both metrics: the centre, then the axis offsets by label (row above, left, right, row
+// below), then the diagonals by label.  One thread per 32-pixel word of a row: the word is written
+// unclaimed, then every set bit of each in-grid neighbour word, lowest priority first, overwrites its
+// pixel (program order keeps the best).  The scatter's result, without the fill or the CAS loops.
+__global__ void seed_bits(uint32_t* __restrict__ bits, int64_t wpr, const uint32_t* __restrict__ seeds, int64_t s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = seeds[i];
+    const uint32_t x = c & 0xFFFFu, y = c >> 16;
+    atomicOr(&bits[(int64_t)y * wpr + (x >> 5)], 1u << (x & 31));
+  }
+}
+__global__ void jfa_first_gather(uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N, int k,
+                                 const uint32_t* __restrict__ bits, int64_t wpr, uint32_t unclaimed, int vn) {
+  const int kw = k >> 5;  // k in words (k >= 32)
+  const int64_t total = (int64_t)rows * wpr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / wpr), w = (int)(t - (int64_t)r * wpr);
+    const int y = row0 + r, x0 = w << 5;
+    uint32_t* out = g + (int64_t)r * pitch + x0;
+    const uint4 u = make_uint4(unclaimed, unclaimed, unclaimed, unclaimed);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) reinterpret_cast<uint4*>(out)[q] = u;
+    // offsets in increasing priority (the last store to a pixel wins): diagonals, axis, centre
+    constexpr int OX[9] = {1, -1, 1, -1, 0, 1, -1, 0, 0};
+    constexpr int OY[9] = {1, 1, -1, -1, 1, 0, 0, -1, 0};
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (vn && OX[i] != 0 && OY[i] != 0) continue;
+      const int qy = y + OY[i] * k, qw = w + OX[i] * kw;
+      if (qy < 0 || qy >= N || qw < 0 || (int64_t)qw >= wpr) continue;
+      uint32_t b = __ldg(bits + (int64_t)qy * wpr + qw);
+      const uint32_t base = ((uint32_t)qy << 16) | (uint32_t)(qw << 5);
+      while (b) {
+        const int j = __ffs(b) - 1;
+        b &= b - 1;
+        out[j] = base | (uint32_t)j;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ dJFA
 // SimulateParticles (Alg. 1): new = clamp(old + disp) per axis (R-10); at
 // N = 65536 the EMPTY pixel (65535, 65535) is reserved -> (65534, 65535) (R-4).

@@ -775,14 +775,17 @@ def test_packed_passes_ragged_grid_bit_exact(vd, N):
     assert max(packed) > 0
 
 
-@pytest.mark.parametrize("env", ["VD_NO_FIRST_SCATTER=1", "VD_NO_SK=1", "VD_NO_FULL=1", "VD_ORDER=1", "VD_NO_FUSE=1",
-                                 "VD_REMAP=1", "VD_NO_TMAP=1", "VD_NO_FIVE=1", "VD_FUSE_PF=0"])
+@pytest.mark.parametrize("env", ["VD_NO_FIRST_SCATTER=1", "VD_FIRST_GATHER=1", "VD_NO_SK=1", "VD_NO_FULL=1",
+                                 "VD_ORDER=1", "VD_NO_FUSE=1", "VD_REMAP=1", "VD_NO_TMAP=1", "VD_NO_FIVE=1",
+                                 "VD_FUSE_PF=0", "VD_NO_RST_FOLD=1", "VD_LAT_ALL=1", "VD_FULL_MIN=4"])
 def test_kernel_variant_switches_bit_exact(vd, env):
     # The A/B switches (read once per process) select the r01 kernels: JFA's init + gather
     # first pass instead of the seed scatter, jump_pass_fast instead of jump_pass_sk, segment
     # walks instead of whole residue classes, the other grid order, the separate remap kernel
     # instead of the remap fused into the first dJFA pass (and the lanes variant of it), six
-    # bulk copies instead of one tensor copy per staged row.  Same labels either way.
+    # bulk copies instead of one tensor copy per staged row, the seed scatter instead of the bitmap
+    # gather for JFA's first pass, the separate fwd reset, the lattice walk below N = 32768 (the
+    # packed form with unclaimed labels), one residue class per FULL walk.  Same labels either way.
     import subprocess, sys, os
     code = (
         "import numpy as np, synth, oracle, paper_2209_00117_b200 as vd\n"
