@@ -167,7 +167,8 @@ struct vd_ctx {
   cudaStream_t halo_stream = nullptr;             // halo exchange overlapped with interior rows
   cudaEvent_t halo_ready = nullptr, halo_done = nullptr;
   cudaEvent_t copy_done = nullptr;
-  uint32_t* fwd = nullptr;        // [N*N] forward map (dJFA), allocated on first use
+  uint32_t* fwd = nullptr;        // forward map (dJFA), allocated on first use: [N x 65536] or [N x N]
+  int fwd_pitch = 0;              // 0: indexed by the label itself; N: by y N + x (vdk::fwd_index)
   uint32_t* bits = nullptr;       // [N * ceil(N/32)] seed bitmap of JFA's first pass, allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
   // Locality flags of one frame (packed-key pass, vd_kernels.cuh): loc[i] = 0 iff every label
@@ -1288,8 +1289,13 @@ vd_status enqueue_label_hash(vd_ctx* h);
 // accumulated by the last pass when it can (jump_pass_sk HASH, k = 1), else by label_hash.
 vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash) {
   NvtxRange range("vd_djfa_step");
-  if (!h->fwd) {  // forward map, kept all-EMPTY between steps; indexed by the label itself ((y << 16) | x)
-    const size_t bytes = (size_t)h->N * 65536 * sizeof(uint32_t);
+  if (!h->fwd) {  // forward map, kept all-EMPTY between steps
+    // indexed by the label itself ((y << 16) | x) where the fused frame can run (one band, Euclidean,
+    // Moore), else by y N + x
+    // (VD_FWD_COMPACT=1: y N + x for every handle, A/B)
+    static const bool compact = [] { const char* e = getenv("VD_FWD_COMPACT"); return e && e[0] == '1'; }();
+    h->fwd_pitch = (!compact && h->metric == 0 && h->world == 1 && h->vshards == 1 && h->vn_waves == 0) ? 0 : (int)h->N;
+    const size_t bytes = (size_t)h->N * (h->fwd_pitch ? h->N : 65536) * sizeof(uint32_t);
     CK(cudaMalloc(&h->fwd, bytes));
     CK(cudaMemsetAsync(h->fwd, 0xFF, bytes, h->stream));
   }
@@ -1315,9 +1321,9 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   // and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
   static const bool no_fuse = [] { const char* e = getenv("VD_NO_FUSE"); return e && e[0] == '1'; }();
   const uint32_t k1 = ks[0];
-  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 &&
+  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->fwd_pitch == 0 &&
                     sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
-  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, (int64_t)h->s, (int)h->N,
+  vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, h->fwd_pitch, (int64_t)h->s, (int)h->N,
                                            fuse ? h->shards[0].buf[h->cur] : nullptr, h->pitch);
   if ((st = after_launch(h, "move_fwd"))) return st;
   CK(cudaEventRecord(h->disp_used[slot], h->stream));
@@ -1346,13 +1352,13 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
       }
       if (h->rst_pending) {  // that pass could not carry it
         h->rst_pending = false;
-        vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->rst_seeds, (int64_t)h->s);
+        vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, h->fwd_pitch, (int)h->N, h->rst_seeds, (int64_t)h->s);
         if ((st = after_launch(h, "fwd_reset"))) return st;
       }
     }
     if (h->rst_pending || ks.size() == 1 || no_fold) {  // no second pass (or the fold is off)
       h->rst_pending = false;
-      vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->rst_seeds, (int64_t)h->s);
+      vdk::fwd_reset<<<gs, 256, 0, h->stream>>>(h->fwd, h->fwd_pitch, (int)h->N, h->rst_seeds, (int64_t)h->s);
       if ((st = after_launch(h, "fwd_reset"))) return st;
     }
     loc_end(h);
@@ -1368,10 +1374,10 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   for (auto& sh : h->shards) {
     if (remap_kind == 1)
       vdk::remap_lanes<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
-                                                                     h->fwd, (int)sh.row0, loc ? h->loc : nullptr);
+                                                                     h->fwd, h->fwd_pitch, (int)sh.row0, loc ? h->loc : nullptr);
     else
       vdk::remap<<<rows_grid(h, sh.rows), 256, 0, h->stream>>>(sh.buf[h->cur], h->pitch, (int)sh.rows, (int)h->N,
-                                                               h->fwd, (int)sh.row0, loc ? h->loc : nullptr);
+                                                               h->fwd, h->fwd_pitch, (int)sh.row0, loc ? h->loc : nullptr);
     if ((st = after_launch(h, "remap"))) return st;
   }
   if ((st = timed_end(h, 0, 0))) return st;
@@ -1379,7 +1385,7 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   // 3. re-stamp the new seed pixels; fwd back to all-EMPTY
   for (size_t g = 0; g < h->shards.size(); ++g) {
     Shard& sh = h->shards[g];
-    vdk::reset_stamp<<<gs, 256, 0, h->stream>>>(h->fwd, (int)h->N, h->seeds, h->seeds_new, sh.buf[h->cur], h->pitch,
+    vdk::reset_stamp<<<gs, 256, 0, h->stream>>>(h->fwd, h->fwd_pitch, (int)h->N, h->seeds, h->seeds_new, sh.buf[h->cur], h->pitch,
                                                 (int)sh.row0, (int)sh.rows, (int64_t)h->s, g == 0 ? 1 : 0);
     if ((st = after_launch(h, "reset_stamp"))) return st;
   }

@@ -48,7 +48,7 @@ struct PassArgs {
                     // 2 = (residue, x-block, segment) (jump_pass_sk_remap only)
   int32_t nwalk;    // jump_pass_sk: > 0 = whole residue classes, nwalk of them per CTA (FULL walks)
   int32_t tmap;     // jump_pass_sk, k >= 256, one band: stage each row's six spans with ONE tensor copy
-  const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label)
+  const uint32_t* fwd;  // jump_pass_sk_remap: the forward map (old seed position -> new label), indexed by the label
   int32_t prefetch;     // jump_pass_sk_remap: also pull the fwd lines of the row after next into L1
   unsigned long long* hash_out;  // jump_pass_sk<1> HASH: add the outputs' label checksum here
   // jump_pass_sk: also restore fwd[rst_seeds[i]] = EMPTY for i < rst_s (the fused dJFA frame's
@@ -955,6 +955,9 @@ __device__ __forceinline__ void stage_walk(const PassArgs& a, const CUtensorMap*
 // HASH (the last pass of an e2e dJFA step, KM = 1): every output label is also added to the
 // frame's checksum, sum over p of fmix32((y N + x) * 0x9E3779B9 ^ label) mod 2^64 (label_hash),
 // so the step needs no separate 4-B/px read for its result.
+__device__ __forceinline__ uint32_t fwd_index(uint32_t c, int fp) {
+  return fp ? c + (c >> 16) * (uint32_t)(fp - 65536) : c;  // y 2^16 + x + y (fp - 2^16) = y fp + x
+}
 #ifndef VD_FWD_HINT
 #define VD_FWD_HINT 0  // 1: the fused pass's fwd gathers carry an L2 evict_last policy (A/B)
 #endif
@@ -1068,7 +1071,7 @@ __device__ __forceinline__ void walk_sk(const PassArgs& a, const CUtensorMap* tm
       uint32_t own = own0 + (uint32_t)(s * k);
       if (FIX && s == 0 && left_out) own += (uint32_t)k;
       if (FIX && s == NS - 1 && right_out) own -= (uint32_t)k;
-      lab[s] = c == EMPTY ? own : ld_fwd(a.fwd + c, fwd_pol);  // (fwd is indexed by the label itself, pitch 2^16)
+      lab[s] = c == EMPTY ? own : ld_fwd(a.fwd + c, fwd_pol);  // (the fused frame's fwd: indexed by the label itself)
     }
   };
   auto consume = [&](int i, R_t& R) {
@@ -1934,6 +1937,9 @@ __global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __r
   }
 }
 
+// fwd's index of label c: the label itself (fp = 0: rows of 2^16 entries, the fused dJFA frame's
+// layout) or (y, x) -> y fp + x (fp = N: the N x N layout of the separate remap's runs, whose gathers
+// then spread over a quarter of the address range at C4; r02c).
 // SimulateParticles (Alg. 1) fused with the forward map (R-9):
 // new = clamp(old + disp) per axis (R-10; the reserved pixel at N = 65536, R-4), then
 // fwd[old] <- min(fwd[old], new): co-located seeds leave the smallest new label.  fwd is indexed
@@ -1943,7 +1949,7 @@ __global__ void move_clamp(const uint32_t* __restrict__ old_s, const short2* __r
 // pass, with EMPTY, which the pass's in-stage remap turns into the pixel's own position (R-9:
 // remap, then re-stamp).  A dJFA diagram holds no EMPTY, so the marker is free.  One band.
 __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __restrict__ disp,
-                         uint32_t* __restrict__ new_s, uint32_t* __restrict__ fwd, int64_t s, int N,
+                         uint32_t* __restrict__ new_s, uint32_t* __restrict__ fwd, int fp, int64_t s, int N,
                          uint32_t* __restrict__ flag_g = nullptr, int64_t pitch = 0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t c = old_s[i];
@@ -1954,7 +1960,7 @@ __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __res
     if (N == 65536 && x == 65535 && y == 65535) x = 65534;
     const uint32_t nw = ((uint32_t)y << 16) | (uint32_t)x;
     new_s[i] = nw;
-    atomicMin(&fwd[c], nw);
+    atomicMin(&fwd[fwd_index(c, fp)], nw);
     if (flag_g) flag_g[(int64_t)y * pitch + x] = EMPTY;  // marker: "new seed here" (jump_pass_sk_remap)
   }
 }
@@ -1962,13 +1968,13 @@ __global__ void move_fwd(const uint32_t* __restrict__ old_s, const short2* __res
 // After the remap: restore fwd to all-EMPTY (its entries at the old seed pixels) and
 // re-stamp the new seed pixels of this band (R-9: remap, then re-stamp).  Co-located seeds
 // write the same values, so the unordered writes are benign.
-__global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s,
+__global__ void reset_stamp(uint32_t* __restrict__ fwd, int fp, int N, const uint32_t* __restrict__ old_s,
                             const uint32_t* __restrict__ new_s, uint32_t* __restrict__ g, int64_t pitch, int row0,
                             int rows, int64_t s, int do_reset) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     if (do_reset) {
       const uint32_t o = old_s[i];
-      fwd[o] = EMPTY;
+      fwd[fwd_index(o, fp)] = EMPTY;
     }
     const uint32_t c = new_s[i];
     const int y = (int)(c >> 16) - row0, x = (int)(c & 0xFFFFu);
@@ -1978,10 +1984,10 @@ __global__ void reset_stamp(uint32_t* __restrict__ fwd, int N, const uint32_t* _
 
 // Fused dJFA frame (NEXT-1), after the first pass: fwd back to all-EMPTY (its entries at the old
 // seed pixels).
-__global__ void fwd_reset(uint32_t* __restrict__ fwd, int N, const uint32_t* __restrict__ old_s, int64_t s) {
+__global__ void fwd_reset(uint32_t* __restrict__ fwd, int fp, int N, const uint32_t* __restrict__ old_s, int64_t s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = old_s[i];
-    fwd[o] = EMPTY;
+    fwd[fwd_index(o, fp)] = EMPTY;
   }
 }
 
@@ -1997,7 +2003,7 @@ constexpr int kRemapUnroll = VD_REMAP_UNROLL;  // row quads in flight per remap 
 // its pixel (hence within Euclidean 63 = kLocR, 44 * sqrt(2) < 63): the packed-key passes'
 // precondition (walk).  Tracked as max over pixels of (cy - y + 44, cx - x + 44) in two
 // 16-bit lanes (a lane outside [0, 88] wraps high).
-__global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd,
+__global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd, int fp,
                       int row0, uint32_t* __restrict__ loc) {
   uint32_t mx = 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -2013,7 +2019,7 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
       for (int e = 0; e < 4; ++e) {
         const uint32_t c = w[e];
         if (x + e < N) {
-          const uint32_t nc = c != EMPTY ? __ldg(fwd + c) : EMPTY;
+          const uint32_t nc = c != EMPTY ? __ldg(fwd + fwd_index(c, fp)) : EMPTY;
           w[e] = nc;
           // (cy - y + 44, cx - x - e + 44); EMPTY is far
           mx = __vmaxu2(mx, nc == EMPTY ? 0xFFFFFFFFu : __vadd2(nc, __vsub2(nbx, (uint32_t)e)));
@@ -2032,7 +2038,7 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
 // remap is latency-bound (a DRAM load of the labels, then a dependent L2 gather of fwd), so
 // each thread loads the labels of its NEXT round before it gathers and stores the current one:
 // the two latencies overlap instead of adding up.  Same result and locality flag as remap().
-__global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd,
+__global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd, int fp,
                             int row0, uint32_t* __restrict__ loc) {
   uint32_t mx = 0;
   const int lane = (int)threadIdx.x & 31, warp = (int)threadIdx.x >> 5, nwarps = (int)blockDim.x >> 5;
@@ -2062,7 +2068,7 @@ __global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, i
     uint32_t nc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      nc[e] = cur[e] != EMPTY ? __ldg(fwd + cur[e]) : EMPTY;
+      nc[e] = cur[e] != EMPTY ? __ldg(fwd + fwd_index(cur[e], fp)) : EMPTY;
     int r, x0;
     round_at(i, r, x0);
     uint32_t* row = g + (int64_t)r * pitch;
