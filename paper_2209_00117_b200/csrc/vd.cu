@@ -168,7 +168,8 @@ struct vd_ctx {
   cudaEvent_t halo_ready = nullptr, halo_done = nullptr;
   cudaEvent_t copy_done = nullptr;
   uint32_t* fwd = nullptr;        // forward map (dJFA), allocated on first use: [N x 65536] or [N x N]
-  int fwd_pitch = 0;              // 0: indexed by the label itself; N: by y N + x (vdk::fwd_index)
+  int fwd_pitch = 0;              // this frame's layout: 0 = indexed by the label itself; N = y N + x (vdk::fwd_index)
+  bool fwd_fusable = false;       // fwd sized N x 65536 (a frame may fuse), else N x N
   uint32_t* bits = nullptr;       // [N * ceil(N/32)] seed bitmap of JFA's first pass, allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
   // Locality flags of one frame (packed-key pass, vd_kernels.cuh): loc[i] = 0 iff every label
@@ -1292,10 +1293,10 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   if (!h->fwd) {  // forward map, kept all-EMPTY between steps
     // indexed by the label itself ((y << 16) | x) where the fused frame can run (one band, Euclidean,
     // Moore), else by y N + x
-    // (VD_FWD_COMPACT=1: y N + x for every handle, A/B)
-    static const bool compact = [] { const char* e = getenv("VD_FWD_COMPACT"); return e && e[0] == '1'; }();
-    h->fwd_pitch = (!compact && h->metric == 0 && h->world == 1 && h->vshards == 1 && h->vn_waves == 0) ? 0 : (int)h->N;
-    const size_t bytes = (size_t)h->N * (h->fwd_pitch ? h->N : 65536) * sizeof(uint32_t);
+    // (the layout is chosen per frame, below; the table is all-EMPTY between frames in both, and is
+    // sized for the label-indexed one only where a frame can fuse)
+    h->fwd_fusable = h->metric == 0 && h->world == 1 && h->vshards == 1 && h->vn_waves == 0;
+    const size_t bytes = (size_t)h->N * (h->fwd_fusable ? 65536 : h->N) * sizeof(uint32_t);
     CK(cudaMalloc(&h->fwd, bytes));
     CK(cudaMemsetAsync(h->fwd, 0xFF, bytes, h->stream));
   }
@@ -1321,8 +1322,12 @@ vd_status djfa_step(vd_ctx* h, const int16_t* disp_xy, uint32_t d_max, bool hash
   // and fwd is reset after that pass.  VD_NO_FUSE=1: the separate remap kernel.
   static const bool no_fuse = [] { const char* e = getenv("VD_NO_FUSE"); return e && e[0] == '1'; }();
   const uint32_t k1 = ks[0];
-  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->fwd_pitch == 0 &&
+  const bool fuse = !no_fuse && loc && h->world == 1 && h->vshards == 1 && h->vn_waves == 0 && h->fwd_fusable &&
                     sk_ok(h, k1, false, false) && k1 >= 4 && k1 <= 128;
+  // fwd indexed by the label itself for the fused pass (one address computation per gather), by
+  // y N + x for the separate remap, whose row-order sweep then gathers over a quarter of the address
+  // range at C4 (0.47 vs 0.72 ms; `profiles/r02c_remap_layout_ab_c4.txt`)
+  h->fwd_pitch = fuse ? 0 : (int)h->N;
   vdk::move_fwd<<<gs, 256, 0, h->stream>>>(h->seeds, dd, h->seeds_new, h->fwd, h->fwd_pitch, (int64_t)h->s, (int)h->N,
                                            fuse ? h->shards[0].buf[h->cur] : nullptr, h->pitch);
   if ((st = after_launch(h, "move_fwd"))) return st;
