@@ -1993,7 +1993,9 @@ __global__ void fwd_reset(uint32_t* __restrict__ fwd, int fp, int N, const uint3
 
 // Reuse VD_{t-1}: every label moves with its seed, labels[p] <- fwd[labels[p]].
 // Neighbouring pixels mostly share a label, so the gathers hit L1.
-// Row-major sweeps below: CTAs stride over rows, threads over 4-label quads of a row, with
+// Row-major sweeps below (launch bounds: 8 CTAs of 256 threads resident per SM, the grid being
+// num_sms x 8: at 36 registers only 7 fit, and the eighth CTA per SM ran as a second, nearly empty
+// wave -- the separate remap took 0.72 instead of 0.47 ms at C4, r02c): CTAs stride over rows, threads over 4-label quads of a row, with
 // the quad loop unrolled so that several 128-bit loads are in flight per thread.
 #ifndef VD_REMAP_UNROLL
 #define VD_REMAP_UNROLL 4
@@ -2003,7 +2005,7 @@ constexpr int kRemapUnroll = VD_REMAP_UNROLL;  // row quads in flight per remap 
 // its pixel (hence within Euclidean 63 = kLocR, 44 * sqrt(2) < 63): the packed-key passes'
 // precondition (walk).  Tracked as max over pixels of (cy - y + 44, cx - x + 44) in two
 // 16-bit lanes (a lane outside [0, 88] wraps high).
-__global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd, int fp,
+__global__ void __launch_bounds__(256, 8) remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd, int fp,
                       int row0, uint32_t* __restrict__ loc) {
   uint32_t mx = 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -2038,7 +2040,7 @@ __global__ void remap(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, 
 // remap is latency-bound (a DRAM load of the labels, then a dependent L2 gather of fwd), so
 // each thread loads the labels of its NEXT round before it gathers and stores the current one:
 // the two latencies overlap instead of adding up.  Same result and locality flag as remap().
-__global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd, int fp,
+__global__ void __launch_bounds__(256, 8) remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, int N, const uint32_t* __restrict__ fwd, int fp,
                             int row0, uint32_t* __restrict__ loc) {
   uint32_t mx = 0;
   const int lane = (int)threadIdx.x & 31, warp = (int)threadIdx.x >> 5, nwarps = (int)blockDim.x >> 5;
@@ -2091,7 +2093,7 @@ __global__ void remap_lanes(uint32_t* __restrict__ g, int64_t pitch, int rows, i
 // ------------------------------------------------------------------ reductions (block_sum_u64 above)
 
 // Eq. 5 numerator: count of pixels with equal labels in a band.
-__global__ void match_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t pitch,
+__global__ void __launch_bounds__(256, 8) match_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t pitch,
                             int rows, int N, unsigned long long* __restrict__ out) {
   uint32_t cnt = 0;  // per thread: at most rows/gridDim * N/blockDim*... < 2^32 for any grid we allow
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -2110,7 +2112,7 @@ __global__ void match_count(const uint32_t* __restrict__ a, const uint32_t* __re
 }
 
 // Number of pixels of a band holding `value` (StF's "fully flooded" test).
-__global__ void count_value(const uint32_t* __restrict__ g, int64_t pitch, int rows, int N, uint32_t value,
+__global__ void __launch_bounds__(256, 8) count_value(const uint32_t* __restrict__ g, int64_t pitch, int rows, int N, uint32_t value,
                             unsigned long long* __restrict__ out) {
   uint32_t cnt = 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -2128,7 +2130,7 @@ __global__ void count_value(const uint32_t* __restrict__ g, int64_t pitch, int r
 
 // Checksum sum_p fmix32((uint32)(p * 0x9E3779B9) ^ label[p]) in uint64 over a band
 // (p = global y*N + x < 2^32).
-__global__ void label_hash(const uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N,
+__global__ void __launch_bounds__(256, 8) label_hash(const uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N,
                            unsigned long long* __restrict__ out) {
   // sum over p of fmix32(p * 0x9E3779B9 ^ label[p]) mod 2^64 (p = y * N + x).  The position
   // term advances by a constant per column, so it costs one add per pixel.
