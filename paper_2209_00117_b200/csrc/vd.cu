@@ -170,7 +170,7 @@ struct vd_ctx {
   uint32_t* fwd = nullptr;        // forward map (dJFA), allocated on first use: [N x 65536] or [N x N]
   int fwd_pitch = 0;              // this frame's layout: 0 = indexed by the label itself; N = y N + x (vdk::fwd_index)
   bool fwd_fusable = false;       // fwd sized N x 65536 (a frame may fuse), else N x N
-  uint32_t* bits = nullptr;       // [N * ceil(N/32)] seed bitmap of JFA's first pass, allocated on first use
+  uint32_t* bits = nullptr;       // 2 x [N * ceil(N/32)] occupancy bitmaps (JFA's sparse passes), allocated on first use
   unsigned long long* counter = nullptr;     // device u64 for reductions
   // Locality flags of one frame (packed-key pass, vd_kernels.cuh): loc[i] = 0 iff every label
   // of the input of the frame's i-th tracked pass lies within kLocR of its pixel.
@@ -1151,13 +1151,14 @@ vd_status jfa_init_first_pass(vd_ctx* h, uint32_t k1, bool vn) {
   if (gather && k1 >= 32) {
     const int64_t wpr = (h->N + 31) / 32;
     const size_t bytes = (size_t)h->N * wpr * sizeof(uint32_t);
-    if (!h->bits) CK(cudaMalloc(&h->bits, bytes));
+    if (!h->bits) CK(cudaMalloc(&h->bits, 2 * bytes));  // (two bitmaps: the sparse passes ping-pong them)
     CK(cudaMemsetAsync(h->bits, 0, bytes, h->stream));
     vdk::seed_bits<<<grid_for(h, (int64_t)h->s, 256), 256, 0, h->stream>>>(h->bits, wpr, h->seeds, (int64_t)h->s);
     vd_status st = after_launch(h, "seed_bits");
     if (st) return st;
     for (auto& sh : h->shards) {
-      vdk::jfa_first_gather<<<grid_for(h, (int64_t)sh.rows * wpr, 256), 256, 0, h->stream>>>(
+      const dim3 gg((unsigned)((wpr + 255) / 256), (unsigned)std::min<int64_t>(sh.rows, (int64_t)h->num_sms * 32));
+      vdk::jfa_first_gather<<<gg, 256, 0, h->stream>>>(
           sh.buf[h->cur], h->pitch, (int)sh.row0, (int)sh.rows, (int)h->N, (int)k1, h->bits, wpr, u, vn ? 1 : 0);
       if ((st = after_launch(h, "jfa_first_gather"))) return st;
     }
@@ -1201,8 +1202,59 @@ vd_status vd_jfa(vd_handle h) {
   bool may_empty = !virt;
   const bool track = may_empty;
   loc_begin(h);  // the passes report locality; once it holds, the rest take the packed-key kernel
+  // Sparse passes (r02c, opt-in VD_SPARSE=1, measured slower): the passes right after the first one,
+  // while their input is mostly EMPTY, read an occupancy bitmap and load labels only where it is set
+  // (one band, Euclidean Moore, N > 32768, N % 128 == 0, lattice keys: k >= N/64).  VD_SPARSE_PASSES=n
+  // sets how many (2: k = N/4 and N/8 at C5, inputs 98% and 94% EMPTY).  C5: 19.2 and 29.3 ms against
+  // 10 ms for the dense lattice passes (`profiles/r02c_sparse_ab_c5.txt`).
+  static const bool no_sparse = [] { const char* e = getenv("VD_SPARSE"); return !(e && e[0] == '1'); }();
+  static const int sparse_n = [] { const char* e = getenv("VD_SPARSE_PASSES"); return e ? atoi(e) : 2; }();
+  const bool sparse_ok = !no_sparse && first == 1 && h->N > 32768 && h->N % 128 == 0 && h->metric == 0 &&
+                         h->world == 1 && h->vshards == 1 && h->jfa_vn_waves == 0 && !h->force_rel && may_empty;
+  const int64_t wpr = (h->N + 31) / 32;
+  int sparse_done = 0;
+  uint32_t* occ_in = nullptr;
+  uint32_t* occ_out = nullptr;
   for (size_t i = first; i < ks.size(); ++i) {
     const bool vn = i < h->jfa_vn_waves;
+    const uint32_t kk = ks[i];
+    if (sparse_ok && sparse_done < sparse_n && (uint64_t)kk * 64 >= h->N && i + 1 < ks.size()) {
+      const size_t bytes = (size_t)h->N * wpr * sizeof(uint32_t);
+      if (!h->bits) CK(cudaMalloc(&h->bits, 2 * bytes));
+      if (sparse_done == 0) {  // the first pass's occupancy, from the seeds it placed
+        occ_in = h->bits;
+        occ_out = h->bits + (size_t)h->N * wpr;
+        CK(cudaMemsetAsync(occ_in, 0, bytes, h->stream));
+        vdk::occ_from_seeds<<<grid_for(h, (int64_t)h->s, 256), 256, 0, h->stream>>>(occ_in, wpr, h->seeds,
+                                                                                  (int64_t)h->s, (int)h->N, (int)ks[0]);
+        if ((st = after_launch(h, "occ_from_seeds"))) return loc_end(h), st;
+      }
+      CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
+      uint32_t lk = 0;
+      while ((1u << lk) < kk) ++lk;
+      Shard& sh = h->shards[0];
+      loc_pass_begin(h, kk);
+      h->pass_loc_ok = false;  // (locality is not reported by this kernel)
+      if ((st = timed_begin(h))) return loc_end(h), st;
+      const bool last_sparse = sparse_done + 1 >= sparse_n;
+      const dim3 gs2((unsigned)((h->N / 4 + 255) / 256), (unsigned)std::min<int64_t>(h->N, (int64_t)h->num_sms * 16));
+      vdk::jfa_sparse_pass<<<gs2, 256, 0, h->stream>>>(
+          sh.buf[h->cur], sh.buf[h->cur ^ 1], h->pitch, (int)h->N, (int)kk, (int)lk, occ_in,
+          last_sparse ? nullptr : occ_out, wpr, h->counter);
+      if ((st = after_launch(h, "jfa_sparse_pass"))) return loc_end(h), st;
+      if ((st = timed_end(h, (uint64_t)h->N * h->N, kk))) return loc_end(h), st;
+      loc_pass_end(h);
+      ++h->pass_seq;
+      h->hpar ^= 1;
+      h->cur ^= 1;
+      h->pushed_k = 0;
+      std::swap(occ_in, occ_out);
+      ++sparse_done;
+      uint64_t any = 1;
+      if ((st = reduce_to_host(h, &any))) return loc_end(h), st;
+      may_empty = any != 0;
+      continue;
+    }
     if (track && may_empty) {
       CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned long long), h->stream));
       h->track_empty = true;

@@ -1894,9 +1894,9 @@ __global__ void seed_bits(uint32_t* __restrict__ bits, int64_t wpr, const uint32
 __global__ void jfa_first_gather(uint32_t* __restrict__ g, int64_t pitch, int row0, int rows, int N, int k,
                                  const uint32_t* __restrict__ bits, int64_t wpr, uint32_t unclaimed, int vn) {
   const int kw = k >> 5;  // k in words (k >= 32)
-  const int64_t total = (int64_t)rows * wpr;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(t / wpr), w = (int)(t - (int64_t)r * wpr);
+  // 2-D grid: blockIdx.x over the words of a row, blockIdx.y strided over rows (no 64-bit division)
+  for (int r = blockIdx.y; r < rows; r += gridDim.y)
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < (int)wpr; w += gridDim.x * blockDim.x) {
     const int y = row0 + r, x0 = w << 5;
     uint32_t* out = g + (int64_t)r * pitch + x0;
     const uint4 u = make_uint4(unclaimed, unclaimed, unclaimed, unclaimed);
@@ -1919,6 +1919,85 @@ __global__ void jfa_first_gather(uint32_t* __restrict__ g, int64_t pitch, int ro
       }
     }
   }
+}
+
+// Sparse JFA passes (r02c): JFA's second and third passes at C5 read inputs that are 94-98% EMPTY.
+// An occupancy bitmap (bit = the pixel holds a label) lets a thread skip the EMPTY candidates: one
+// thread per four pixels of a row (a warp = 128 pixels = four bitmap words) reads the nine candidate
+// nibbles and loads labels only where a nibble is set.  Keys in lattice units (§5.6: every label is
+// congruent to its pixel mod 2k, N <= 64k): (a^2 + b^2, b + 128, a + 128) packed in 32 bits.  The pass
+// also writes its output's bitmap for the next sparse pass.
+__global__ void occ_from_seeds(uint32_t* __restrict__ bits, int64_t wpr, const uint32_t* __restrict__ seeds,
+                               int64_t s, int N, int k) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = seeds[i];
+    const int sx = (int)(c & 0xFFFFu), sy = (int)(c >> 16);
+#pragma unroll
+    for (int oy = -1; oy <= 1; ++oy)
+#pragma unroll
+      for (int ox = -1; ox <= 1; ++ox) {  // the pixels of JFA's first pass that this seed claims
+        const int px = sx - ox * k, py = sy - oy * k;
+        if (px >= 0 && px < N && py >= 0 && py < N) atomicOr(&bits[(int64_t)py * wpr + (px >> 5)], 1u << (px & 31));
+      }
+  }
+}
+__global__ void __launch_bounds__(256) jfa_sparse_pass(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                       int64_t pitch, int N, int k, int lk,
+                                                       const uint32_t* __restrict__ bits_in, uint32_t* __restrict__ bits_out,
+                                                       int64_t wpr, unsigned long long* empty_flag) {
+  // 2-D grid: blockIdx.x over quads of a row, blockIdx.y strided over rows (no 64-bit division);
+  // N / 4 is a multiple of 32, so every lane of a warp runs the same iterations
+  const int per_row = N >> 2;
+  const int lane = (int)threadIdx.x & 31;
+  bool any_e = false;
+  for (int y = blockIdx.y; y < N; y += gridDim.y)
+  for (int xq = blockIdx.x * blockDim.x + threadIdx.x; xq < per_row; xq += gridDim.x * blockDim.x) {
+    const int x = xq << 2;
+    uint32_t best[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll
+    for (int oy = -1; oy <= 1; ++oy) {
+      const int qy = y + oy * k;
+      if (qy < 0 || qy >= N) continue;
+#pragma unroll
+      for (int ox = -1; ox <= 1; ++ox) {
+        const int qx = x + ox * k;
+        if (qx < 0 || qx >= N) continue;
+        const uint32_t nib = (__ldg(bits_in + (int64_t)qy * wpr + (qx >> 5)) >> (qx & 31)) & 0xFu;
+        if (nib == 0u) continue;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + (int64_t)qy * pitch + qx));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (!((nib >> e) & 1u)) continue;
+          const uint32_t c = w[e];
+          const int a = ((int)(c & 0xFFFFu) - (x + e)) >> lk, b = ((int)(c >> 16) - y) >> lk;  // exact (lattice)
+          const uint32_t key = ((uint32_t)(a * a + b * b) << 16) | ((uint32_t)(b + 128) << 8) | (uint32_t)(a + 128);
+          best[e] = min(best[e], key);
+        }
+      }
+    }
+    uint32_t o[4], onib = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (best[e] == 0xFFFFFFFFu) {
+        o[e] = EMPTY;
+        any_e = true;
+      } else {
+        const int a = (int)(best[e] & 0xFFu) - 128, b = (int)((best[e] >> 8) & 0xFFu) - 128;
+        o[e] = ((uint32_t)(y + (b << lk)) << 16) | (uint32_t)(x + e + (a << lk));
+        onib |= 1u << e;
+      }
+    }
+    *reinterpret_cast<uint4*>(out + (int64_t)y * pitch + x) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (bits_out != nullptr) {  // eight lanes = one 32-pixel word of the output's bitmap
+      uint32_t wv = onib << ((lane & 7) * 4);
+      wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 1);
+      wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 2);
+      wv |= __shfl_xor_sync(0xFFFFFFFFu, wv, 4);
+      if ((lane & 7) == 0) bits_out[(int64_t)y * wpr + (x >> 5)] = wv;
+    }
+  }
+  if (empty_flag != nullptr && __any_sync(0xFFFFFFFFu, any_e) && lane == 0) atomicOr(empty_flag, 1ull);
 }
 
 // ------------------------------------------------------------------ dJFA
