@@ -15,7 +15,8 @@
  *           EMPTY = 0xFFFFFFFF (R-4).  At N = 65536 the pixel (65535,65535) is reserved.
  *   diagram row-major N x N labels, rows padded to a pitch that is a multiple of 32
  *           labels (128 B); two ping-pong buffers (gather passes, R-12).
- *   seeds   uint32 labels [s]; plus a direct-mapped forward map fwd[N x N] used by dJFA.
+ *   seeds   uint32 labels [s]; plus a direct-mapped forward map used by dJFA (N x 65536, indexed
+ *           by the label itself, where a frame fuses its remap into the first pass; else N x N).
  * Host arrays crossing the ABI are dense (no pitch): seeds_xy / disp_xy are interleaved
  * x0,y0,x1,y1,...; label maps are N*N row-major (or the rank's band of rows).
  *
